@@ -1,0 +1,198 @@
+// ref_dump — TEST INFRASTRUCTURE. Drives the real reference core (compiled
+// from /root/reference/proj/src by oracle/Makefile, never copied) and writes
+// its outputs in the exact-text formats the parity tests diff against:
+//
+//   ref_dump gen  COUNT RATE PDIST RDIST ADIST SEED PRELOADED OUT.hex
+//   ref_dump mix  BASE.hex REPL.hex FRACTION SEED OUT.hex
+//   ref_dump run  TRACE.hex CFG RECORDS_OUT EVENTS_OUT|-
+//   ref_dump capacity TRACE.hex CFG
+//   ref_dump time TRACE.hex CFG REPEATS            (CPU baseline timing)
+//   ref_dump report TRACE.hex CFG PREFIX           (build_report + write_report)
+//
+// Trace files use the lossless hex-float format "pascal-trace-hex-v1"
+// (one line per request: id arrival(%a) prompt reasoning answering preloaded).
+// CFG is key=value lines for RunConfig (proj/include/pascalsim/engine.hpp:18-33)
+// and LatencyProfile (proj/include/pascalsim/costmodel.hpp:12-21) fields;
+// numbers go through strtod so "%a" hex floats and "inf" are accepted.
+//
+// Record dump line (one per request, id order), all doubles as %a:
+//   R id arrival prefill_complete reasoning_end first_answer_delivery
+//     first_answer_iter_start blocked_interval_total completion
+//     NMIG (start end)* NDEL delivery* NDIG digest*
+// (fields of metrics::RequestRecord, proj/include/pascalsim/metrics.hpp:15-28)
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "pascalsim/engine.hpp"
+#include "pascalsim/metrics.hpp"
+#include "pascalsim/workload.hpp"
+
+using namespace pascalsim;
+
+namespace {
+
+workload::Trace read_hex_trace(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("cannot open " + path);
+    std::string line;
+    std::getline(in, line);
+    if (line != "pascal-trace-hex-v1") throw std::runtime_error("bad hex trace header");
+    workload::Trace t;
+    while (std::getline(in, line)) {
+        if (line.empty()) continue;
+        std::istringstream ls(line);
+        std::string arr;
+        workload::RequestSpec r;
+        int pre = 0;
+        ls >> r.id >> arr >> r.prompt_tokens >> r.reasoning_tokens >> r.answering_tokens >> pre;
+        r.arrival_time = std::strtod(arr.c_str(), nullptr);
+        r.kv_preloaded = pre != 0;
+        t.push_back(r);
+    }
+    return t;
+}
+
+void write_hex_trace(const workload::Trace& t, const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw std::runtime_error("cannot write " + path);
+    std::fprintf(f, "pascal-trace-hex-v1\n");
+    for (const auto& r : t)
+        std::fprintf(f, "%ld %a %ld %ld %ld %d\n", r.id, r.arrival_time, r.prompt_tokens,
+                     r.reasoning_tokens, r.answering_tokens, r.kv_preloaded ? 1 : 0);
+    std::fclose(f);
+}
+
+struct Cfg {
+    engine::RunConfig rc;
+    costmodel::LatencyProfile prof;
+};
+
+Cfg read_cfg(const std::string& path) {
+    Cfg c;
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("cannot open " + path);
+    std::string line;
+    while (std::getline(in, line)) {
+        auto eq = line.find('=');
+        if (eq == std::string::npos) continue;
+        std::string k = line.substr(0, eq), v = line.substr(eq + 1);
+        double d = std::strtod(v.c_str(), nullptr);
+        long l = std::strtol(v.c_str(), nullptr, 10);
+        if (k == "instance_count") c.rc.instance_count = static_cast<int>(l);
+        else if (k == "gpu_capacity") c.rc.gpu_capacity = l;
+        else if (k == "capacity_fraction") c.rc.capacity_fraction = d;
+        else if (k == "token_quantum") c.rc.token_quantum = l;
+        else if (k == "demotion_threshold") c.rc.demotion_threshold = l;
+        else if (k == "policy") c.rc.policy = engine::parse_policy(v);
+        else if (k == "no_migration") c.rc.ablations.no_migration = l != 0;
+        else if (k == "non_adaptive") c.rc.ablations.non_adaptive = l != 0;
+        else if (k == "target_tpot") c.rc.target_tpot = d;
+        else if (k == "ttfat_target") c.rc.ttfat_target = d;
+        else if (k == "qoe_threshold") c.rc.qoe_threshold = d;
+        else if (k == "pacer_slack_tokens") c.rc.pacer_slack_tokens = l;
+        else costmodel::profile_set_field(c.prof, k, d);
+    }
+    return c;
+}
+
+void dump_records(const std::vector<metrics::RequestRecord>& recs, FILE* f) {
+    for (const auto& r : recs) {
+        std::fprintf(f, "R %ld %a %a %a %a %a %a %a %zu", r.spec.id, r.arrival,
+                     r.prefill_complete, r.reasoning_end, r.first_answer_delivery,
+                     r.first_answer_iter_start, r.blocked_interval_total, r.completion,
+                     r.migration_intervals.size());
+        for (auto& [s, e] : r.migration_intervals) std::fprintf(f, " %a %a", s, e);
+        std::fprintf(f, " %zu", r.answer_delivery_times.size());
+        for (double d : r.answer_delivery_times) std::fprintf(f, " %a", d);
+        std::fprintf(f, " %zu", r.answer_digest_times.size());
+        for (double d : r.answer_digest_times) std::fprintf(f, " %a", d);
+        std::fprintf(f, "\n");
+    }
+}
+
+int usage() {
+    std::fprintf(stderr, "usage: see header of oracle/ref_dump.cpp\n");
+    return 2;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 2) return usage();
+    std::string mode = argv[1];
+    try {
+        if (mode == "gen" && argc == 10) {
+            using workload::LengthDistribution;
+            auto t = workload::generate_trace(
+                std::strtol(argv[2], nullptr, 10), std::strtod(argv[3], nullptr),
+                LengthDistribution::parse(argv[4]), LengthDistribution::parse(argv[5]),
+                LengthDistribution::parse(argv[6]), std::strtoull(argv[7], nullptr, 10),
+                std::atoi(argv[8]) != 0);
+            write_hex_trace(t, argv[9]);
+        } else if (mode == "mix" && argc == 7) {
+            auto t = workload::mix_traces(read_hex_trace(argv[2]), read_hex_trace(argv[3]),
+                                          std::strtod(argv[4], nullptr),
+                                          std::strtoull(argv[5], nullptr, 10));
+            write_hex_trace(t, argv[6]);
+        } else if (mode == "run" && argc == 6) {
+            auto t = read_hex_trace(argv[2]);
+            Cfg c = read_cfg(argv[3]);
+            std::ofstream log;
+            std::ostream* logp = nullptr;
+            if (std::strcmp(argv[5], "-") != 0) {
+                log.open(argv[5]);
+                logp = &log;
+            }
+            auto recs = engine::run(t, c.rc, c.prof, logp);
+            FILE* f = std::fopen(argv[4], "w");
+            if (!f) throw std::runtime_error("cannot write records");
+            dump_records(recs, f);
+            std::fclose(f);
+        } else if (mode == "capacity" && argc == 4) {
+            auto t = read_hex_trace(argv[2]);
+            Cfg c = read_cfg(argv[3]);
+            std::printf("%ld\n", engine::derive_capacity(t, c.rc, c.prof));
+        } else if (mode == "time" && argc == 5) {
+            auto t = read_hex_trace(argv[2]);
+            Cfg c = read_cfg(argv[3]);
+            int reps = std::atoi(argv[4]);
+            using clk = std::chrono::steady_clock;
+            auto t0 = clk::now();
+            long cap = engine::derive_capacity(t, c.rc, c.prof);
+            auto t1 = clk::now();
+            engine::RunConfig rc = c.rc;
+            rc.gpu_capacity = cap;  // run-only: capacity pre-derived
+            double run_s = 0.0;
+            for (int i = 0; i < reps; ++i) {
+                auto a = clk::now();
+                auto recs = engine::run(t, rc, c.prof);
+                auto b = clk::now();
+                run_s += std::chrono::duration<double>(b - a).count();
+                if (recs.size() != t.size()) throw std::runtime_error("lost records");
+            }
+            std::printf("{\"capacity\": %ld, \"derive_s\": %.6f, \"run_s\": %.6f, \"reps\": %d}\n",
+                        cap, std::chrono::duration<double>(t1 - t0).count(), run_s / reps, reps);
+        } else if (mode == "report" && argc == 5) {
+            auto t = read_hex_trace(argv[2]);
+            Cfg c = read_cfg(argv[3]);
+            auto recs = engine::run(t, c.rc, c.prof);
+            auto rep = metrics::build_report(recs, c.rc.target_tpot, c.rc.qoe_threshold,
+                                             c.rc.ttfat_target);
+            metrics::write_report(rep, argv[4]);
+        } else {
+            return usage();
+        }
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "ref_dump: %s\n", e.what());
+        return 1;
+    }
+    return 0;
+}
