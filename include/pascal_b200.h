@@ -1,0 +1,107 @@
+/* pascal_b200.h — additive entry points of libpascal.so (B200 build).
+ *
+ * None of these exist in the reference; they sit beside the 19 drop-in
+ * symbols of pascal.h without changing them (SURVEY.md §8b "Additive
+ * extension"). They serve the replica sweep (many independent simulations
+ * per GPU, one process per GPU), the parity tests (full per-request records
+ * and the decision log in exact-text form) and the benchmark (device-resident
+ * batches timed with CUDA events).
+ */
+#ifndef PASCAL_B200_H
+#define PASCAL_B200_H
+
+#include "pascal.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One replica's outcome: metrics::build_report aggregates
+ * (proj/src/metrics.cpp:115-153) computed on the device, plus the work
+ * counters used for roofline accounting. */
+typedef struct {
+    double ttft_mean, ttft_p50, ttft_p90, ttft_p95, ttft_p99;
+    double slo_violation_rate, ttfat_attainment, throughput;
+    long long capacity;            /* resolved per-instance KV capacity */
+    long long requests;
+    long long request_iterations;  /* prefills + decode participations */
+    long long answer_tokens;
+    long long events, plans, candidate_visits, health_checks;
+    long long slo_violations;
+    int status;                    /* pascal_status of this replica */
+    int pad;
+} pascal_summary;
+
+/* Device-side timing of the most recent batch execution on this thread. */
+typedef struct {
+    double derive_ms;   /* oracle pre-run (engine.cpp:449-471) */
+    double engine_ms;   /* policy run */
+    double metrics_ms;  /* per-request metrics + per-replica summary */
+    double total_ms;    /* whole device step (CUDA events on the launch stream) */
+    double h2d_ms, d2h_ms;
+    long long h2d_bytes, d2h_bytes;
+    int kernel_launches;
+    int pad;
+} pascal_timing;
+
+typedef struct pascal_batch pascal_batch;
+
+/* Uploads `count` replicas (trace k under cfgs[k] / profiles[k]) to the
+ * current device. Inputs are borrowed. */
+pascal_status pascal_batch_create(const pascal_trace* const* traces,
+                                  const pascal_profile* const* profiles,
+                                  const pascal_run_config* cfgs, size_t count,
+                                  pascal_batch** out);
+/* Runs every replica to completion on the device (capacity derivation,
+ * policy run, metrics); inputs stay resident. */
+pascal_status pascal_batch_execute(pascal_batch* b);
+/* Copies the per-replica summaries to host memory. */
+pascal_status pascal_batch_summaries(pascal_batch* b, pascal_summary* out);
+void pascal_batch_free(pascal_batch* b);
+
+/* create + execute + summaries + free: the end-to-end replica-sweep call
+ * with host buffers. */
+pascal_status pascal_run_batch(const pascal_trace* const* traces,
+                               const pascal_profile* const* profiles,
+                               const pascal_run_config* cfgs, size_t count,
+                               pascal_summary* out);
+
+pascal_status pascal_last_timing(pascal_timing* out);
+
+/* Parity: per-request records in the hex-float dump format of
+ * oracle/ref_dump.cpp (id order) and, when event_log_path is non-NULL, the
+ * pascal-events-v1 decision log. */
+pascal_status pascal_run_dump(const pascal_trace* t, const pascal_profile* p,
+                              const pascal_run_config* cfg, const char* records_path,
+                              const char* event_log_path);
+
+/* engine::derive_capacity (proj/src/engine.cpp:449-471), oracle pre-run on
+ * the device. */
+pascal_status pascal_derive_capacity(const pascal_trace* t, const pascal_profile* p,
+                                     const pascal_run_config* cfg, long* out);
+
+/* Lossless trace files (one line per request, arrival as %a). */
+pascal_status pascal_trace_load_hex(const char* path, pascal_trace** out);
+pascal_status pascal_trace_save_hex(const pascal_trace* t, const char* path);
+
+/* Array views for bindings. */
+pascal_status pascal_trace_from_arrays(long n, const long* ids, const double* arrivals,
+                                       const long* prompt, const long* reasoning,
+                                       const long* answering, const int* preloaded,
+                                       pascal_trace** out);
+pascal_status pascal_trace_get(const pascal_trace* t, long i, long* id, double* arrival,
+                               long* prompt, long* reasoning, long* answering,
+                               int* preloaded);
+/* Request-iterations of the trace: sum(R + A - [R==0 and not preloaded] +
+ * [not preloaded]). */
+long long pascal_trace_request_iterations(const pascal_trace* t);
+
+/* One process per GPU: selects the CUDA device for this thread. */
+pascal_status pascal_set_device(int device);
+/* 1 when a usable CUDA device is present (no kernels are launched). */
+int pascal_device_available(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PASCAL_B200_H */

@@ -1,0 +1,298 @@
+"""Python mirror of the reference's public C interface for the scheduling path.
+
+Names, argument meaning and error behaviour follow /root/reference/proj/
+include/pascal.h (trace / profile / run / report / compare), so tests read like
+the reference's own (proj/tests/test_capi.cpp). Every call goes through
+libpascal.so; simulations run on the GPU (sm_100a kernels in csrc/).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Iterable, List, Optional, Sequence
+
+from . import _lib
+
+POLICIES = ("fcfs", "rr", "oracle", "pascal")
+
+# Length presets of the reference CLI (proj/tools/pascalsim_cli.cpp:41-49).
+PRESETS = {
+    "reasoning-char": ("constant:128", "uniform:128:2048", "constant:1", False),
+    "answering-char": ("constant:128", "constant:0", "uniform:128:2048", True),
+    "chat": ("uniform:64:512",
+             "hist:256=0.35,512=0.30,768=0.20,1024=0.10,1536=0.04,2048=0.01",
+             "uniform:256:1024", False),
+    "reasoning-heavy": ("uniform:64:512", "uniform:2048:8192", "uniform:128:512", False),
+}
+
+
+class PascalError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"[status {status}] {message}")
+        self.status = status
+        self.message = message
+
+
+def _lib_():
+    return _lib.load()
+
+
+def _check(status: int) -> None:
+    if status != _lib.OK:
+        msg = _lib_().pascal_last_error()
+        raise PascalError(status, msg.decode() if msg else "")
+
+
+def _b(s: Optional[str]) -> Optional[bytes]:
+    return None if s is None else os.fsencode(s)
+
+
+class Trace:
+    """Opaque pascal_trace handle."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib_().pascal_trace_free(h)
+            self._h = None
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    @classmethod
+    def generate(cls, count: int, arrival_rate: float, prompt: str, reasoning: str,
+                 answering: str, seed: int, kv_preloaded: bool = False) -> "Trace":
+        out = C.c_void_p()
+        _check(_lib_().pascal_trace_generate(count, arrival_rate, _b(prompt), _b(reasoning),
+                                             _b(answering), seed, int(kv_preloaded),
+                                             C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def preset(cls, name: str, count: int, arrival_rate: float, seed: int,
+               mix_fraction: float = 0.25) -> "Trace":
+        """`pascalsim gen --preset` (proj/tools/pascalsim_cli.cpp:169-222)."""
+        if name == "mixed":
+            base = cls.preset("chat", count, arrival_rate, seed)
+            heavy = cls.preset("reasoning-heavy", count, arrival_rate, seed + 1)
+            return cls.mix(base, heavy, mix_fraction, seed + 2)
+        p, r, a, pre = PRESETS[name]
+        return cls.generate(count, arrival_rate, p, r, a, seed, pre)
+
+    @classmethod
+    def mix(cls, base: "Trace", replacement: "Trace", fraction: float, seed: int) -> "Trace":
+        out = C.c_void_p()
+        _check(_lib_().pascal_trace_mix(base._h, replacement._h, fraction, seed, C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def load(cls, path: str) -> "Trace":
+        out = C.c_void_p()
+        _check(_lib_().pascal_trace_load(_b(path), C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def load_hex(cls, path: str) -> "Trace":
+        out = C.c_void_p()
+        _check(_lib_().pascal_trace_load_hex(_b(path), C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def from_arrays(cls, ids, arrivals, prompt, reasoning, answering, preloaded=None) -> "Trace":
+        n = len(ids)
+        L = C.c_long * n
+        D = C.c_double * n
+        I = C.c_int * n
+        out = C.c_void_p()
+        pre = I(*[int(x) for x in preloaded]) if preloaded is not None else None
+        _check(_lib_().pascal_trace_from_arrays(
+            n, L(*ids), D(*arrivals), L(*prompt), L(*reasoning), L(*answering), pre,
+            C.byref(out)))
+        return cls(out.value)
+
+    def save(self, path: str) -> None:
+        _check(_lib_().pascal_trace_save(self._h, _b(path)))
+
+    def save_hex(self, path: str) -> None:
+        _check(_lib_().pascal_trace_save_hex(self._h, _b(path)))
+
+    def __len__(self) -> int:
+        return int(_lib_().pascal_trace_size(self._h))
+
+    def request_iterations(self) -> int:
+        return int(_lib_().pascal_trace_request_iterations(self._h))
+
+    def specs(self) -> List[tuple]:
+        lib = _lib_()
+        out = []
+        i_, p_, r_, a_ = C.c_long(), C.c_long(), C.c_long(), C.c_long()
+        t_ = C.c_double()
+        pre = C.c_int()
+        for k in range(len(self)):
+            _check(lib.pascal_trace_get(self._h, k, C.byref(i_), C.byref(t_), C.byref(p_),
+                                        C.byref(r_), C.byref(a_), C.byref(pre)))
+            out.append((i_.value, t_.value, p_.value, r_.value, a_.value, bool(pre.value)))
+        return out
+
+
+class Profile:
+    """Opaque pascal_profile handle (LatencyProfile, costmodel.hpp:12-21)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib_().pascal_profile_free(h)
+            self._h = None
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    @classmethod
+    def default(cls, **fields) -> "Profile":
+        out = C.c_void_p()
+        _check(_lib_().pascal_profile_default(C.byref(out)))
+        p = cls(out.value)
+        for k, v in fields.items():
+            p.set(k, v)
+        return p
+
+    @classmethod
+    def load(cls, path: str) -> "Profile":
+        out = C.c_void_p()
+        _check(_lib_().pascal_profile_load(_b(path), C.byref(out)))
+        return cls(out.value)
+
+    def save(self, path: str) -> None:
+        _check(_lib_().pascal_profile_save(self._h, _b(path)))
+
+    def set(self, key: str, value: float) -> None:
+        _check(_lib_().pascal_profile_set(self._h, _b(key), float(value)))
+
+    def calibrate(self, samples_path: str) -> float:
+        rmse = C.c_double()
+        _check(_lib_().pascal_profile_calibrate(_b(samples_path), self._h, C.byref(rmse)))
+        return rmse.value
+
+
+def run_config(policy: str = "pascal", **fields) -> _lib.RunConfig:
+    """pascal_run_config with the reference defaults (pascal_run_config_init)."""
+    cfg = _lib.RunConfig()
+    _lib_().pascal_run_config_init(C.byref(cfg))
+    cfg.policy = policy.encode()
+    for k, v in fields.items():
+        if not hasattr(cfg, k):
+            raise AttributeError(k)
+        setattr(cfg, k, v)
+    return cfg
+
+
+def run(trace: Trace, profile: Profile, cfg, report_prefix: str,
+        event_log: Optional[str] = None) -> None:
+    """pascal_run: simulate on the GPU, write the pascal-report-v1 files."""
+    _check(_lib_().pascal_run(trace.handle, profile.handle, C.byref(cfg), _b(report_prefix),
+                              _b(event_log)))
+
+
+def run_dump(trace: Trace, profile: Profile, cfg, records_path: str,
+             event_log: Optional[str] = None) -> None:
+    """Full per-request records (hex-float dump) + optional decision log."""
+    _check(_lib_().pascal_run_dump(trace.handle, profile.handle, C.byref(cfg),
+                                   _b(records_path), _b(event_log)))
+
+
+def derive_capacity(trace: Trace, profile: Profile, cfg) -> int:
+    out = C.c_long()
+    _check(_lib_().pascal_derive_capacity(trace.handle, profile.handle, C.byref(cfg),
+                                          C.byref(out)))
+    return out.value
+
+
+class Report:
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib_().pascal_report_free(h)
+            self._h = None
+
+    @classmethod
+    def load(cls, prefix: str) -> "Report":
+        out = C.c_void_p()
+        _check(_lib_().pascal_report_load(_b(prefix), C.byref(out)))
+        return cls(out.value)
+
+    def summary_value(self, key: str) -> float:
+        out = C.c_double()
+        _check(_lib_().pascal_report_summary_value(self._h, _b(key), C.byref(out)))
+        return out.value
+
+
+def compare(prefixes: Sequence[str], names: Sequence[str], out_path: str) -> None:
+    n = len(prefixes)
+    P = C.c_char_p * max(n, 1)
+    _check(_lib_().pascal_compare(P(*[_b(p) for p in prefixes]), P(*[_b(x) for x in names]),
+                                  n, _b(out_path)))
+
+
+def _arrays(traces, profiles, cfgs):
+    n = len(traces)
+    T = C.c_void_p * n
+    R = _lib.RunConfig * n
+    return n, T(*[t.handle.value for t in traces]), T(*[p.handle.value for p in profiles]), \
+        R(*cfgs)
+
+
+class Batch:
+    """Device-resident replica batch (pascal_batch_*)."""
+
+    def __init__(self, traces: Sequence[Trace], profiles: Sequence[Profile], cfgs: Sequence):
+        n, tt, pp, cc = _arrays(traces, profiles, cfgs)
+        out = C.c_void_p()
+        _check(_lib_().pascal_batch_create(tt, pp, cc, n, C.byref(out)))
+        self._h = out
+        self.n = n
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib_().pascal_batch_free(h)
+            self._h = None
+
+    def execute(self) -> None:
+        _check(_lib_().pascal_batch_execute(self._h))
+
+    def summaries(self) -> List[_lib.Summary]:
+        out = (_lib.Summary * self.n)()
+        _check(_lib_().pascal_batch_summaries(self._h, out))
+        return list(out)
+
+
+def run_batch(traces, profiles, cfgs) -> List[_lib.Summary]:
+    n, tt, pp, cc = _arrays(traces, profiles, cfgs)
+    out = (_lib.Summary * n)()
+    _check(_lib_().pascal_run_batch(tt, pp, cc, n, out))
+    return list(out)
+
+
+def last_timing() -> _lib.Timing:
+    t = _lib.Timing()
+    _check(_lib_().pascal_last_timing(C.byref(t)))
+    return t
+
+
+def set_device(device: int) -> None:
+    _check(_lib_().pascal_set_device(device))
+
+
+def device_available() -> bool:
+    return bool(_lib_().pascal_device_available())

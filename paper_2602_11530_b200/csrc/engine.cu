@@ -1,0 +1,1369 @@
+// engine.cu — the B200 scheduling engine (sm_100a).
+//
+// Replaces, end to end, the reference's per-iteration scheduling loop:
+//   event loop          proj/src/engine.cpp:392-404        -> run_replica()
+//   arrival placement   engine.cpp:260-283, cluster.cpp:10-33,59-62
+//   monitor snapshot    instance.cpp:22-33,59-76, engine.cpp:103-109
+//   demotion            instance.cpp:39-57
+//   planner             instance.cpp:103-282               -> plan_and_apply()
+//   plan application    engine.cpp:192-258
+//   iteration retire    engine.cpp:310-337, instance.cpp:10-20
+//   phase boundary      engine.cpp:159-190, cluster.cpp:35-57,64-68
+//   other handlers      engine.cpp:285-308,339-367
+//
+// Execution model: one warp owns one replica for its whole lifetime. Scalar
+// simulation state (clock, counters, heap size) is held redundantly and
+// identically by all 32 lanes; data-parallel steps (queue scans, stable
+// priority partition, plan materialisation, batch retire, snapshots) spread
+// over the lanes with ballots, prefix scans and shuffles.
+//
+// Bit-exactness: built with -fmad=false; every floating-point expression keeps
+// the reference's operation order (see the costmodel helpers below).
+//
+// The admission pass is the reference's greedy admit/evict loop with the
+// O(Q) two-pointer victim walk: victim order is exactly the
+// reverse of admission order, so the victims of an admission are (a) not yet
+// visited candidates taken from the back, then (b) previously denied residents
+// in descending order (a stack), restricted to the class-eligible suffix.
+
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+
+#include "engine.h"
+
+namespace pb {
+
+#define DEVI __device__ __forceinline__
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------- meta bits
+constexpr unsigned PH_WAIT = 0, PH_REASON = 1, PH_ANSWER = 2, PH_DONE = 3;
+constexpr unsigned LOC_GPU = 0, LOC_CPU = 1, LOC_TRANSIT = 2;
+DEVI unsigned m_phase(unsigned m) { return m & 3u; }
+DEVI unsigned m_loc(unsigned m) { return (m >> 2) & 3u; }
+DEVI bool m_swin(unsigned m) { return (m >> 4) & 1u; }
+DEVI bool m_swout(unsigned m) { return (m >> 5) & 1u; }
+DEVI bool m_qlow(unsigned m) { return (m >> 6) & 1u; }
+DEVI int m_owner(unsigned m) { return (int)(m >> 8); }
+DEVI unsigned m_set_phase(unsigned m, unsigned p) { return (m & ~3u) | p; }
+DEVI unsigned m_set_loc(unsigned m, unsigned l) { return (m & ~(3u << 2)) | (l << 2); }
+DEVI unsigned m_set_swin(unsigned m, bool b) { return (m & ~(1u << 4)) | ((unsigned)b << 4); }
+DEVI unsigned m_set_swout(unsigned m, bool b) { return (m & ~(1u << 5)) | ((unsigned)b << 5); }
+DEVI unsigned m_set_qlow(unsigned m, bool b) { return (m & ~(1u << 6)) | ((unsigned)b << 6); }
+DEVI unsigned m_set_owner(unsigned m, int o) { return (m & 0xffu) | ((unsigned)o << 8); }
+// instance.hpp:59-61
+DEVI bool m_resident(unsigned m) { return m_loc(m) == LOC_GPU && !m_swin(m) && !m_swout(m); }
+// instance.cpp:86-90 (a queued request is never Done)
+DEVI bool m_candidate(unsigned m) {
+    return m_phase(m) != PH_DONE && m_loc(m) != LOC_TRANSIT && !m_swin(m) && !m_swout(m);
+}
+
+// candidate flags (int4::w of the candidate scratch)
+constexpr int CF_LOW = 1, CF_WAIT = 2, CF_RES = 4, CF_QPOS = 8;
+// candidate status
+constexpr unsigned char CS_ADMIT = 1, CS_DENY = 2;
+
+// event kinds in the heap key
+constexpr unsigned EV_PREFILL = 1, EV_ITER = 2, EV_SWAP = 3, EV_TRANSFER = 4;
+
+// ------------------------------------------------------------- warp helpers
+DEVI int lane_id() { return threadIdx.x & 31; }
+DEVI unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+DEVI long long warp_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+DEVI int warp_sum(int v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+DEVI unsigned warp_min_u(unsigned v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+}
+DEVI unsigned warp_max_u(unsigned v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+}
+DEVI int warp_excl_scan(int v, int* total) {
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULL, x, o);
+        if (lane_id() >= o) x += y;
+    }
+    *total = __shfl_sync(FULL, x, 31);
+    return x - v;
+}
+// Lowest key, ties to the lowest id (argmin_by's strict '<' in id order,
+// proj/src/cluster.cpp:10-23).
+DEVI void warp_argmin(long long& key, int& id) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        long long k2 = __shfl_xor_sync(FULL, key, o);
+        int i2 = __shfl_xor_sync(FULL, id, o);
+        if (k2 < key || (k2 == key && i2 < id)) {
+            key = k2;
+            id = i2;
+        }
+    }
+}
+
+// -------------------------------------------------------------- costmodel
+// proj/src/costmodel.cpp:35-51, operation order preserved (device code is
+// compiled with -fmad=false so no contraction happens).
+DEVI double prefill_latency(const Profile& p, long long prompt) {
+    return __dadd_rn(p.prefill_base, __dmul_rn(p.prefill_per_token, (double)prompt));
+}
+DEVI double decode_step_latency(const Profile& p, long long batch, long long kv) {
+    return __dadd_rn(__dadd_rn(p.decode_base, __dmul_rn(p.decode_per_request, (double)batch)),
+                     __dmul_rn(p.decode_per_kv_token, (double)kv));
+}
+DEVI double swap_latency(const Profile& p, long long kv) {
+    if (kv == 0) return 0.0;
+    return __ddiv_rn((double)kv, p.swap_bandwidth);
+}
+DEVI double transfer_latency(const Profile& p, long long kv) {
+    return __dadd_rn(p.fabric_latency, __ddiv_rn((double)kv, p.fabric_bandwidth));
+}
+DEVI double dmax(double a, double b) { return a < b ? b : a; }  // std::max(a, b)
+
+// ------------------------------------------------------- per-replica view
+struct Inst {  // shared-memory SoA for the replica's instances
+    long long* gpu;
+    long long* cpu;
+    double* iter_start;
+    double* link;
+    int* hi_len;
+    int* lo_len;
+    int* hcount;
+    int* lcount;
+    int* afresh;
+    int* blen;
+    int* busy;
+    int* healthy;
+};
+
+struct Rep {
+    int n, ni, policy, flags;
+    long long cap, quantum, demotion, slack;
+    double tpot;
+    Profile prof;
+    long long logcap;
+    // request arrays (offset to this replica)
+    const double* arrival;
+    const int4* spec;
+    const long long* aoff;
+    int4* hot;
+    unsigned* meta;
+    int* qused;
+    int* ndel;
+    int* cursor;
+    RecOut* rec;
+    double* dig;
+    double* del;
+    uint2* qent;
+    long long qcap;
+    unsigned* batch;
+    HeapEnt* heap;
+    int4* cand;
+    int4* tmp;
+    unsigned* tmpq;
+    unsigned char* cstat;
+    unsigned* elist;
+    unsigned* stack;
+    LogEnt* log;
+    Inst s;
+};
+
+struct Scal {
+    double now;
+    unsigned long long evseq;
+    unsigned enq;
+    int next_arr;
+    int hn;
+    int done;
+    int status;
+    long long gpu_total, peak, nlog;
+    long long events, plans, visits, req_iters, ans_tokens, health;
+};
+
+DEVI uint2* queue_ptr(const Rep& R, int i, int low) {
+    return R.qent + (long long)(2 * i + low) * R.qcap;
+}
+
+// ------------------------------------------------------------- event log
+DEVI void log_put(const Rep& R, long long pos, double t, int kind, int inst, int req, int det) {
+    if ((R.flags & kLogEvents) && pos < R.logcap) {
+        LogEnt e;
+        e.t = t;
+        e.req = req;
+        e.inst = inst;
+        e.kind = kind;
+        e.detail = det;
+        R.log[pos] = e;
+    }
+}
+// Scalar emit (engine.cpp:91-97): one line at the end of the log.
+DEVI void emit(const Rep& R, Scal& S, int kind, int inst, int req, int det = 0) {
+    if (lane_id() == 0) log_put(R, S.nlog, S.now, kind, inst, req, det);
+    S.nlog++;
+}
+
+// ------------------------------------------------------------ event heap
+// Min-heap on (time, seq) == EventAfter (engine.cpp:52-57). 1-based; lane 0
+// does the memory work, every lane tracks hn.
+DEVI bool ev_less(double ta, unsigned long long ka, double tb, unsigned long long kb) {
+    return ta < tb || (ta == tb && ka < kb);
+}
+DEVI void heap_push(const Rep& R, Scal& S, double t, unsigned kind, unsigned id) {
+    // engine.cpp:85-89
+    if (t < S.now - 1e-12) {
+        if (S.status == 0) S.status = kErrPast;
+        return;
+    }
+    unsigned long long key = ((++S.evseq) << 29) | ((unsigned long long)kind << 26) | id;
+    int pos = ++S.hn;
+    if (lane_id() == 0) {
+        HeapEnt* h = R.heap;
+        while (pos > 1) {
+            int p = pos >> 1;
+            HeapEnt pe = h[p];
+            if (!ev_less(t, key, pe.t, pe.key)) break;
+            h[pos] = pe;
+            pos = p;
+        }
+        h[pos].t = t;
+        h[pos].key = key;
+    }
+    __syncwarp();
+}
+DEVI HeapEnt heap_pop(const Rep& R, Scal& S) {
+    HeapEnt top;
+    int n = S.hn;
+    if (lane_id() == 0) {
+        HeapEnt* h = R.heap;
+        top = h[1];
+        HeapEnt last = h[n];
+        int m = n - 1;
+        int i = 1;
+        while (true) {
+            int c = 2 * i;
+            if (c > m) break;
+            HeapEnt cl = h[c];
+            if (c + 1 <= m) {
+                HeapEnt cr = h[c + 1];
+                if (ev_less(cr.t, cr.key, cl.t, cl.key)) {
+                    cl = cr;
+                    ++c;
+                }
+            }
+            if (!ev_less(cl.t, cl.key, last.t, last.key)) break;
+            h[i] = cl;
+            i = c;
+        }
+        if (m >= 1) h[i] = last;
+    }
+    top.t = __shfl_sync(FULL, top.t, 0);
+    top.key = __shfl_sync(FULL, top.key, 0);
+    S.hn = n - 1;
+    __syncwarp();
+    return top;
+}
+
+// ------------------------------------------------------------ queues
+// Queue (instance i, class low) is an append-only array of {idx, seq}; an
+// entry is live iff hot[idx].seq == seq (dequeue zeroes the request's seq).
+// Live entries keep ascending-seq order, i.e. the order of the reference's
+// std::vector queues (engine.cpp:111-126).
+DEVI void queue_compact(const Rep& R, int i, int low) {
+    uint2* q = queue_ptr(R, i, low);
+    int len = low ? R.s.lo_len[i] : R.s.hi_len[i];
+    int w = 0;
+    for (int base = 0; base < len; base += 32) {
+        int k = base + lane_id();
+        bool live = false;
+        uint2 e = make_uint2(0, 0);
+        if (k < len) {
+            e = q[k];
+            live = (unsigned)R.hot[e.x].z == e.y;
+        }
+        unsigned mk = __ballot_sync(FULL, live);
+        __syncwarp();
+        if (live) q[w + __popc(mk & lanemask_lt())] = e;
+        w += __popc(mk);
+    }
+    __syncwarp();
+    if (lane_id() == 0) {
+        if (low) R.s.lo_len[i] = w;
+        else R.s.hi_len[i] = w;
+    }
+    __syncwarp();
+}
+
+// engine.cpp:111-116 (+ monitor counters r_i / a_i kept incrementally)
+DEVI void enqueue(const Rep& R, Scal& S, int i, int idx, bool high) {
+    int len = high ? R.s.hi_len[i] : R.s.lo_len[i];
+    if (len >= R.qcap) {
+        queue_compact(R, i, high ? 0 : 1);
+        len = high ? R.s.hi_len[i] : R.s.lo_len[i];
+    }
+    unsigned seq = ++S.enq;
+    if (lane_id() == 0) {
+        int4 h = R.hot[idx];
+        h.z = (int)seq;
+        R.hot[idx] = h;
+        unsigned m = R.meta[idx];
+        m = m_set_owner(m_set_qlow(m, !high), i);
+        R.meta[idx] = m;
+        queue_ptr(R, i, high ? 0 : 1)[len] = make_uint2((unsigned)idx, seq);
+        if (high) {
+            R.s.hi_len[i] = len + 1;
+            R.s.hcount[i] += 1;
+        } else {
+            R.s.lo_len[i] = len + 1;
+            R.s.lcount[i] += 1;
+            if (h.w == 0) R.s.afresh[i] += 1;
+        }
+    }
+    __syncwarp();
+}
+
+// engine.cpp:122-126 (lane 0 only; caller syncs)
+DEVI void dequeue_lane(const Rep& R, int idx, int owner, unsigned m, int quanta) {
+    int4 h = R.hot[idx];
+    h.z = 0;
+    R.hot[idx] = h;
+    if (m_qlow(m)) {
+        atomicSub(&R.s.lcount[owner], 1);
+        if (quanta == 0) atomicSub(&R.s.afresh[owner], 1);
+    } else {
+        atomicSub(&R.s.hcount[owner], 1);
+    }
+}
+
+// ------------------------------------------------------ monitor snapshots
+// PacerState::healthy (instance.cpp:22-33) with a monotone cursor: `now`
+// never decreases, so the count of digests <= now only grows.
+DEVI bool pacer_healthy(const Rep& R, Scal& S, int idx, int answering) {
+    int nd = R.ndel[idx];
+    if (nd == 0) return true;
+    const double* d = R.dig + R.aoff[idx];
+    double t0 = d[0];
+    long long expected = 1 + (long long)floor(__ddiv_rn(__dsub_rn(S.now, t0), R.tpot));
+    if (expected > answering) expected = answering;
+    int c = R.cursor[idx];
+    while (c < nd && d[c] <= S.now) ++c;
+    R.cursor[idx] = c;
+    return (long long)c >= expected - R.slack;
+}
+
+// t_i for every instance (instance.cpp:67-74): AND over low-queue Answering
+// members. Results go to R.s.healthy[].
+DEVI void compute_health(const Rep& R, Scal& S) {
+    long long checks = 0;
+    for (int i = 0; i < R.ni; ++i) {
+        uint2* q = queue_ptr(R, i, 1);
+        int len = R.s.lo_len[i];
+        bool ok = true;
+        for (int base = 0; base < len && ok; base += 32) {
+            int k = base + lane_id();
+            bool bad = false;
+            bool chk = false;
+            if (k < len) {
+                uint2 e = q[k];
+                int4 h = R.hot[e.x];
+                if ((unsigned)h.z == e.y) {
+                    unsigned m = R.meta[e.x];
+                    if (m_phase(m) == PH_ANSWER) {
+                        chk = true;
+                        bad = !pacer_healthy(R, S, (int)e.x, R.spec[e.x].z);
+                    }
+                }
+            }
+            checks += __popc(__ballot_sync(FULL, chk));
+            ok = __ballot_sync(FULL, bad) == 0;
+        }
+        if (lane_id() == 0) R.s.healthy[i] = ok ? 1 : 0;
+    }
+    S.health += checks;
+    __syncwarp();
+}
+
+// Alg. 1 / baseline routing (cluster.cpp:27-33,59-62): argmin m_i, healthy
+// instances first when `health` is set.
+DEVI int select_by_m(const Rep& R, bool health) {
+    long long bk = LLONG_MAX;
+    int bid = INT_MAX;
+    for (int pass = 0; pass < (health ? 2 : 1) && bid == INT_MAX; ++pass) {
+        bool only_healthy = health && pass == 0;
+        for (int base = 0; base < R.ni; base += 32) {
+            int i = base + lane_id();
+            long long k = LLONG_MAX;
+            int id = INT_MAX;
+            if (i < R.ni && (!only_healthy || R.s.healthy[i])) {
+                k = R.s.gpu[i] + R.s.cpu[i];
+                id = i;
+            }
+            warp_argmin(k, id);
+            if (k < bk || (k == bk && id < bid)) {
+                bk = k;
+                bid = id;
+            }
+        }
+    }
+    return bid;
+}
+
+// Alg. 2 (cluster.cpp:35-44): healthy argmin r_i, else argmin r_i + a_i.
+DEVI int select_answering(const Rep& R) {
+    long long bk = LLONG_MAX;
+    int bid = INT_MAX;
+    for (int pass = 0; pass < 2 && bid == INT_MAX; ++pass) {
+        for (int base = 0; base < R.ni; base += 32) {
+            int i = base + lane_id();
+            long long k = LLONG_MAX;
+            int id = INT_MAX;
+            if (i < R.ni && (pass == 1 || R.s.healthy[i])) {
+                k = pass == 0 ? (long long)R.s.hcount[i]
+                              : (long long)R.s.hcount[i] + (long long)R.s.afresh[i];
+                id = i;
+            }
+            warp_argmin(k, id);
+            if (k < bk || (k == bk && id < bid)) {
+                bk = k;
+                bid = id;
+            }
+        }
+    }
+    return bid;
+}
+
+// ------------------------------------------------------------- handlers
+DEVI void add_gpu(const Rep& R, Scal& S, int i, long long d) {
+    if (lane_id() == 0) R.s.gpu[i] += d;
+    S.gpu_total += d;
+}
+DEVI void add_cpu(const Rep& R, int i, long long d) {
+    if (lane_id() == 0) R.s.cpu[i] += d;
+}
+DEVI void note_peak(Scal& S) {  // engine.cpp:75-79
+    if (S.gpu_total > S.peak) S.peak = S.gpu_total;
+}
+
+// engine.cpp:159-190 (Pascal branch; the caller has already set phase,
+// reasoning_end and logged "transition").
+DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
+    unsigned m = R.meta[idx];
+    int4 h = R.hot[idx];
+    int cur = m_owner(m);
+    if (lane_id() == 0) dequeue_lane(R, idx, cur, m, h.w);
+    __syncwarp();
+    compute_health(R, S);
+    int target = select_answering(R);
+    long long kv = h.x;
+    // cluster.cpp:46-57
+    bool migrate;
+    if (R.flags & kNoMigration) migrate = false;
+    else if (target == cur) migrate = false;
+    else if (R.flags & kNonAdaptive) migrate = true;
+    else {
+        long long cur_free = R.cap - R.s.gpu[cur];
+        long long tgt_free = R.cap - R.s.gpu[target];
+        migrate = !(cur_free >= kv && tgt_free < kv);
+    }
+    if (!migrate) {
+        if (lane_id() == 0) {
+            R.qused[idx] = 0;
+            int4 hh = R.hot[idx];
+            hh.w = 0;
+            R.hot[idx] = hh;
+        }
+        __syncwarp();
+        enqueue(R, S, cur, idx, false);
+        return;
+    }
+    // free_memory (engine.cpp:128-133) on the current owner
+    unsigned loc = m_loc(m);
+    if (loc == LOC_GPU || m_swin(m)) add_gpu(R, S, cur, -kv);
+    else if (loc == LOC_CPU) add_cpu(R, cur, -kv);
+    double dur = transfer_latency(R.prof, kv);
+    double busy = R.s.link[target];
+    double start = dmax(S.now, busy);  // cluster.cpp:64-68
+    double fin = __dadd_rn(start, dur);
+    if (lane_id() == 0) {
+        R.s.link[target] = fin;
+        R.meta[idx] = m_set_owner(m_set_loc(m, LOC_TRANSIT), target);
+        RecOut* rc = &R.rec[idx];
+        rc->mig_start = S.now;
+        rc->mig_end = fin;
+        rc->nmig = 1;
+    }
+    __syncwarp();
+    heap_push(R, S, fin, EV_TRANSFER, (unsigned)idx);
+    emit(R, S, kLMigrate, cur, idx, target);
+}
+
+// Shared by the R == 0 path of prefill completion: a single answer delivery
+// (PacerState::on_delivery, instance.cpp:10-20 + engine.cpp:148-156).
+DEVI void deliver_lane(const Rep& R, double now, int idx, double iter_start) {
+    int nd = R.ndel[idx];
+    double* d = R.dig + R.aoff[idx];
+    double v = nd == 0 ? now : dmax(now, __dadd_rn(d[nd - 1], R.tpot));
+    d[nd] = v;
+    if (R.flags & kRecordDeliv) R.del[R.aoff[idx] + nd] = now;
+    R.ndel[idx] = nd + 1;
+    if (nd == 0) {
+        R.rec[idx].first_answer_delivery = now;
+        R.rec[idx].first_answer_iter_start = iter_start;
+    }
+}
+
+// ----------------------------------------------------------- the planner
+// Admission walk helpers. `b` is the lowest index visited by the back walk:
+// every resident (rkv > 0) candidate at index >= b has been evicted.
+struct Adm {
+    long long free_;
+    int b;
+    int ns;  // stack size
+    int ne;  // evictions
+};
+
+DEVI int cand_rkv(int4 c) { return ((c.w & CF_RES) && c.z > 0) ? c.z : 0; }
+
+// Walk the unvisited back region down to `lo` while need > free (or free < 0
+// when need < 0 encodes the over-capacity repair). Victims are taken highest
+// index first (instance.cpp:166-177 reversed order == candidate order).
+DEVI void walk_back(const Rep& R, Adm& A, int lo, long long need) {
+    while (A.b > lo && need > A.free_) {
+        int w0 = max(lo, A.b - 32);
+        int cnt = A.b - w0;
+        int rkv = 0;
+        unsigned idx = 0;
+        if (lane_id() < cnt) {
+            int4 c = R.cand[w0 + lane_id()];
+            rkv = cand_rkv(c);
+            idx = (unsigned)c.x;
+        }
+        unsigned mk = __ballot_sync(FULL, rkv > 0);
+        int newb = w0;
+        while (mk && need > A.free_) {
+            int j = 31 - __clz(mk);
+            mk &= ~(1u << j);
+            long long kv = __shfl_sync(FULL, rkv, j);
+            unsigned vi = __shfl_sync(FULL, idx, j);
+            A.free_ += kv;
+            if (lane_id() == 0) R.elist[A.ne] = vi;
+            A.ne++;
+            newb = w0 + j;
+        }
+        // if still short the whole window was consumed
+        A.b = need > A.free_ ? w0 : newb;
+    }
+}
+DEVI void pop_stack(const Rep& R, Adm& A, int s, long long need) {
+    while (A.ns > 0 && need > A.free_) {
+        int j = (int)R.stack[A.ns - 1];
+        if (j < s) break;
+        A.ns--;
+        int4 c = R.cand[j];
+        A.free_ += c.z;
+        if (lane_id() == 0) R.elist[A.ne] = (unsigned)c.x;
+        A.ne++;
+    }
+}
+
+// Gather one queue into tmp (and optionally demote first). Returns the number
+// of candidates appended at tmp[*nt..]; tracks min/max quanta.
+DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned& qmin,
+                       unsigned& qmax) {
+    uint2* q = queue_ptr(R, i, low);
+    int len = low ? R.s.lo_len[i] : R.s.hi_len[i];
+    const bool demote = (R.policy == kPascal) && !low;
+    int w = 0;
+    for (int base = 0; base < len; base += 32) {
+        int k = base + lane_id();
+        bool live = false, dem = false, cnd = false;
+        uint2 e = make_uint2(0, 0);
+        int4 h = make_int4(0, 0, 0, 0);
+        unsigned m = 0;
+        if (k < len) {
+            e = q[k];
+            h = R.hot[e.x];
+            live = (unsigned)h.z == e.y;
+            if (live) {
+                m = R.meta[e.x];
+                dem = demote && (long long)h.x > R.demotion;  // strict, instance.cpp:44
+            }
+        }
+        // --- demotion (instance.cpp:39-57): new seqs in queue order, appended
+        // to the low queue; logged "demote" in that order (engine.cpp:196-197).
+        unsigned dm = __ballot_sync(FULL, dem);
+        if (dm) {
+            int nd = __popc(dm);
+            int lo_len = R.s.lo_len[i];
+            if (lo_len + nd > R.qcap) {
+                queue_compact(R, i, 1);
+                lo_len = R.s.lo_len[i];
+            }
+            int rank = __popc(dm & lanemask_lt());
+            if (dem) {
+                unsigned seq = S.enq + 1 + rank;
+                h.z = (int)seq;
+                h.w = 0;
+                R.hot[e.x] = h;
+                R.qused[e.x] = 0;
+                m = m_set_qlow(m, true);
+                R.meta[e.x] = m;
+                queue_ptr(R, i, 1)[lo_len + rank] = make_uint2(e.x, seq);
+                log_put(R, S.nlog + rank, S.now, kLDemote, i, (int)e.x, 0);
+            }
+            __syncwarp();
+            if (lane_id() == 0) {
+                R.s.lo_len[i] = lo_len + nd;
+                R.s.hcount[i] -= nd;
+                R.s.lcount[i] += nd;
+                R.s.afresh[i] += nd;
+            }
+            S.enq += nd;
+            S.nlog += nd;
+            __syncwarp();
+        }
+        bool keep = live && !dem;
+        cnd = keep && m_candidate(m);
+        // compact the queue in place (tombstones and demoted entries leave)
+        unsigned km = __ballot_sync(FULL, keep);
+        __syncwarp();
+        if (keep) q[w + __popc(km & lanemask_lt())] = e;
+        w += __popc(km);
+        // candidate record
+        unsigned cm = __ballot_sync(FULL, cnd);
+        if (cnd) {
+            int flags = (low ? CF_LOW : 0);
+            int need;
+            if (m_phase(m) == PH_WAIT) {  // instance.cpp:94-99
+                int4 sp = R.spec[e.x];
+                flags |= CF_WAIT;
+                need = sp.x + (sp.y == 0 ? 1 : 0);
+                if (m_resident(m)) flags |= CF_RES;
+            } else if (m_resident(m)) {
+                flags |= CF_RES;
+                need = 1;
+            } else {
+                need = h.x + 1;
+            }
+            if (h.w > 0) flags |= CF_QPOS;
+            int pos = nt + __popc(cm & lanemask_lt());
+            R.tmp[pos] = make_int4((int)e.x, need, h.x, flags);
+            R.tmpq[pos] = (unsigned)h.w;
+        }
+        unsigned qv = cnd ? (unsigned)h.w : 0xffffffffu;
+        qmin = min(qmin, warp_min_u(qv));
+        qmax = max(qmax, warp_max_u(cnd ? (unsigned)h.w : 0u));
+        nt += __popc(cm);
+    }
+    __syncwarp();
+    if (lane_id() == 0) {
+        if (low) R.s.lo_len[i] = w;
+        else R.s.hi_len[i] = w;
+    }
+    __syncwarp();
+}
+
+// Stable partition of tmp[s, e) by quanta ascending into cand[s, e)
+// (== sort by (quanta, enqueue_seq) since queues are in seq order).
+DEVI void order_segment(const Rep& R, int s, int e, unsigned qmin, unsigned qmax, bool by_quanta) {
+    if (!by_quanta || qmin >= qmax) {
+        for (int k = s + lane_id(); k < e; k += 32) R.cand[k] = R.tmp[k];
+        __syncwarp();
+        return;
+    }
+    int out = s;
+    unsigned q = qmin;
+    while (true) {
+        unsigned next = 0xffffffffu;
+        for (int base = s; base < e; base += 32) {
+            int k = base + lane_id();
+            unsigned kq = 0xffffffffu;
+            if (k < e) kq = R.tmpq[k];
+            bool sel = kq == q;
+            unsigned sm = __ballot_sync(FULL, sel);
+            if (sel) R.cand[out + __popc(sm & lanemask_lt())] = R.tmp[k];
+            out += __popc(sm);
+            next = min(next, warp_min_u(kq > q ? kq : 0xffffffffu));
+        }
+        if (next == 0xffffffffu) break;
+        q = next;
+    }
+    __syncwarp();
+}
+
+// maybe_start (engine.cpp:192-258) with plan_iteration (instance.cpp:103-282).
+DEVI void maybe_start(const Rep& R, Scal& S, int i) {
+    if (R.s.busy[i]) return;
+    S.plans++;
+    const bool pascal = R.policy == kPascal;
+    const bool classed = pascal;
+
+    // ---- gather (+ demotion) and priority order (instance.cpp:113-141)
+    int nt = 0;
+    unsigned qmin0 = 0xffffffffu, qmax0 = 0, qmin1 = 0xffffffffu, qmax1 = 0;
+    gather_queue(R, S, i, 0, nt, qmin0, qmax0);
+    int c1 = nt;
+    if (pascal) gather_queue(R, S, i, 1, nt, qmin1, qmax1);
+    const int n = nt;
+    S.visits += n;
+    const bool by_quanta = R.policy == kRr || pascal;
+    if (pascal) {
+        order_segment(R, 0, c1, qmin0, qmax0, true);
+        order_segment(R, c1, n, qmin1, qmax1, true);
+    } else {
+        order_segment(R, 0, n, qmin0, qmax0, by_quanta);
+    }
+    // k0: first class-0 candidate with quanta > 0 (victims of a class-0
+    // admission form the suffix [k0, n), instance.cpp:158-162)
+    int k0 = c1;
+    if (classed) {
+        for (int base = 0; base < c1; base += 32) {
+            int k = base + lane_id();
+            bool qp = k < c1 && (R.cand[k].w & CF_QPOS);
+            unsigned mk = __ballot_sync(FULL, qp);
+            if (mk) {
+                k0 = base + __ffs(mk) - 1;
+                break;
+            }
+        }
+    }
+
+    // ---- admission / controlled preemption (instance.cpp:143-243)
+    Adm A;
+    A.free_ = R.cap - R.s.gpu[i];
+    A.b = n;
+    A.ns = 0;
+    A.ne = 0;
+    bool any_admitted = false, fcfs_blocked = false;
+    const bool fcfs = R.policy == kFcfs, oracle = R.policy == kOracle;
+    for (int base = 0; base < n; base += 32) {
+        int4 my = make_int4(0, 0, 0, 0);
+        if (base + lane_id() < n) my = R.cand[base + lane_id()];
+        unsigned char st = 0;
+        int cnt = min(32, n - base);
+        for (int k = 0; k < cnt; ++k) {
+            int ci = base + k;
+            int cx = __shfl_sync(FULL, my.x, k);
+            long long need = __shfl_sync(FULL, my.y, k);
+            int cz = __shfl_sync(FULL, my.z, k);
+            int cw = __shfl_sync(FULL, my.w, k);
+            int rkv = ((cw & CF_RES) && cz > 0) ? cz : 0;
+            unsigned char dec;
+            if ((ci >= A.b && rkv > 0) || (fcfs_blocked && rkv == 0)) {
+                dec = CS_DENY;  // evicted earlier in this pass, or FCFS strict queue
+            } else {
+                if (need > A.free_) {
+                    bool allow = !oracle && !(fcfs && (cw & CF_WAIT));
+                    if (allow) {
+                        int s = classed ? ((cw & CF_LOW) ? c1 : k0) : 0;
+                        walk_back(R, A, max(s, ci + 1), need);
+                        pop_stack(R, A, s, need);
+                        if (need > A.free_ && !any_admitted) {  // deadlock breaker :211-220
+                            walk_back(R, A, ci + 1, need);
+                            pop_stack(R, A, 0, need);
+                        }
+                    }
+                }
+                if (need <= A.free_) {
+                    dec = CS_ADMIT;
+                    any_admitted = true;
+                    A.free_ -= need;
+                } else {
+                    dec = CS_DENY;
+                    if (rkv > 0) {
+                        if (lane_id() == 0) R.stack[A.ns] = (unsigned)ci;
+                        A.ns++;
+                    }
+                    if (fcfs) fcfs_blocked = true;
+                }
+            }
+            (void)cx;
+            if (lane_id() == k) st = dec;
+        }
+        if (base + lane_id() < n) R.cstat[base + lane_id()] = st;
+        __syncwarp();
+    }
+    if (A.free_ < 0) pop_stack(R, A, 0, 0);  // over-capacity repair :235-243
+
+    // ---- materialise (instance.cpp:245-281): pass A, statistics
+    int pf = INT_MAX;
+    long long bcount = 0, bkv = 0;
+    int nsw = 0, nimm = 0, nden = 0;
+    for (int base = 0; base < n; base += 32) {
+        int k = base + lane_id();
+        bool adm = false, den = false, wt = false, inb = false, sw = false, imm = false;
+        int4 c = make_int4(0, 0, 0, 0);
+        if (k < n) {
+            c = R.cand[k];
+            unsigned char st = R.cstat[k];
+            adm = st == CS_ADMIT;
+            den = st == CS_DENY;
+        }
+        if (adm) {
+            if (c.w & CF_WAIT) wt = true;
+            else if (c.w & CF_RES) inb = true;
+            else if (swap_latency(R.prof, c.z) == 0.0) { imm = true; inb = true; }
+            else sw = true;
+        }
+        unsigned wm = __ballot_sync(FULL, wt);
+        if (wm && pf == INT_MAX) pf = base + __ffs(wm) - 1;
+        bcount += __popc(__ballot_sync(FULL, inb));
+        bkv += warp_sum_ll(inb ? (long long)c.z : 0);
+        nsw += __popc(__ballot_sync(FULL, sw));
+        nimm += __popc(__ballot_sync(FULL, imm));
+        nden += __popc(__ballot_sync(FULL, den));
+    }
+    int kind;  // 0 idle, 1 prefill, 2 decode
+    double dur;
+    int pf_idx = -1;
+    if (pf != INT_MAX) {
+        pf_idx = R.cand[pf].x;
+        kind = 1;
+        dur = prefill_latency(R.prof, R.spec[pf_idx].x);
+    } else if (bcount > 0) {
+        kind = 2;
+        dur = decode_step_latency(R.prof, bcount, bkv);
+    } else {
+        kind = 0;
+        dur = 0.0;
+    }
+
+    // ---- apply (engine.cpp:201-257). Evictions first, in eviction order.
+    long long log0 = S.nlog;
+    for (int base = 0; base < A.ne; base += 32) {
+        int k = base + lane_id();
+        bool act = k < A.ne;
+        long long kv = 0;
+        double sd = 0.0;
+        int vi = 0;
+        if (act) {
+            vi = (int)R.elist[k];
+            int4 h = R.hot[vi];
+            kv = h.x;
+            unsigned m = m_set_loc(R.meta[vi], LOC_CPU);
+            sd = swap_latency(R.prof, kv);
+            if (sd > 0.0) m = m_set_swout(m, true);
+            R.meta[vi] = m;
+            log_put(R, log0 + k, S.now, kLEvict, i, vi, 0);
+        }
+        long long tot = warp_sum_ll(kv);
+        add_gpu(R, S, i, -tot);
+        add_cpu(R, i, tot);
+        unsigned pm = __ballot_sync(FULL, act && sd > 0.0);
+        while (pm) {
+            int j = __ffs(pm) - 1;
+            pm &= pm - 1;
+            double t = __shfl_sync(FULL, sd, j);
+            int v = __shfl_sync(FULL, vi, j);
+            heap_push(R, S, __dadd_rn(S.now, t), EV_SWAP, (unsigned)v);
+        }
+    }
+    __syncwarp();
+    // pass B: swap-ins, immediate swap-ins, denials, batch, in candidate order
+    long long lsw = log0 + A.ne, limm = lsw + nsw, lden = limm + nimm;
+    int bpos = 0;
+    unsigned* bout = R.batch + (long long)i * R.n;
+    for (int base = 0; base < n; base += 32) {
+        int k = base + lane_id();
+        bool adm = false, den = false, inb = false, sw = false, imm = false;
+        int4 c = make_int4(0, 0, 0, 0);
+        if (k < n) {
+            c = R.cand[k];
+            unsigned char st = R.cstat[k];
+            adm = st == CS_ADMIT;
+            den = st == CS_DENY;
+        }
+        double sd = 0.0;
+        if (adm && !(c.w & CF_WAIT)) {
+            if (c.w & CF_RES) inb = true;
+            else {
+                sd = swap_latency(R.prof, c.z);
+                if (sd == 0.0) { imm = true; inb = true; }
+                else sw = true;
+            }
+        }
+        unsigned swm = __ballot_sync(FULL, sw), imm_m = __ballot_sync(FULL, imm),
+                 dnm = __ballot_sync(FULL, den), bm = __ballot_sync(FULL, inb);
+        unsigned lt = lanemask_lt();
+        if (sw) {
+            unsigned m = R.meta[c.x];
+            R.meta[c.x] = m_set_swin(m, true);
+            log_put(R, lsw + __popc(swm & lt), S.now, kLSwapIn, i, c.x, 0);
+        }
+        if (imm) {
+            unsigned m = R.meta[c.x];
+            R.meta[c.x] = m_set_loc(m, LOC_GPU);
+            log_put(R, limm + __popc(imm_m & lt), S.now, kLSwapIn, i, c.x, 0);
+        }
+        if (den) {
+            RecOut* rc = &R.rec[c.x];
+            rc->blocked = __dadd_rn(rc->blocked, dur);
+            log_put(R, lden + __popc(dnm & lt), S.now, kLBlock, i, c.x, 0);
+        }
+        if (inb && kind == 2) bout[bpos + __popc(bm & lt)] = (unsigned)c.x;
+        long long mv = warp_sum_ll((sw || imm) ? (long long)c.z : 0);
+        add_cpu(R, i, -mv);
+        add_gpu(R, S, i, mv);
+        lsw += __popc(swm);
+        limm += __popc(imm_m);
+        lden += __popc(dnm);
+        bpos += __popc(bm);
+        while (swm) {
+            int j = __ffs(swm) - 1;
+            swm &= swm - 1;
+            double t = __shfl_sync(FULL, sd, j);
+            int v = __shfl_sync(FULL, c.x, j);
+            heap_push(R, S, __dadd_rn(S.now, t), EV_SWAP, (unsigned)v);
+        }
+    }
+    S.nlog = log0 + A.ne + nsw + nimm + nden;
+    __syncwarp();
+
+    if (kind == 1) {
+        int4 sp = R.spec[pf_idx];
+        add_gpu(R, S, i, (long long)sp.x + (sp.y == 0 ? 1 : 0));
+        if (lane_id() == 0) {
+            R.s.busy[i] = 1;
+            R.s.iter_start[i] = S.now;
+            R.s.blen[i] = 0;
+        }
+        __syncwarp();
+        heap_push(R, S, __dadd_rn(S.now, dur), EV_PREFILL, (unsigned)pf_idx);
+        emit(R, S, kLPrefillStart, i, pf_idx);
+    } else if (kind == 2) {
+        add_gpu(R, S, i, bcount);  // growth reserved up front (engine.cpp:245)
+        if (lane_id() == 0) {
+            R.s.busy[i] = 1;
+            R.s.iter_start[i] = S.now;
+            R.s.blen[i] = (int)bcount;
+        }
+        __syncwarp();
+        heap_push(R, S, __dadd_rn(S.now, dur), EV_ITER, (unsigned)i);
+        emit(R, S, kLDecodeStart, i, -1, (int)bcount);
+    }
+    __syncwarp();
+    if (R.s.gpu[i] > R.cap && S.status == 0) S.status = kErrCapacity;
+    note_peak(S);
+}
+
+// --------------------------------------------------------------- events
+// engine.cpp:260-283
+DEVI void on_arrival(const Rep& R, Scal& S, int idx) {
+    if (lane_id() == 0) R.rec[idx].arrival = S.now;
+    const bool pascal = R.policy == kPascal;
+    if (pascal) compute_health(R, S);
+    int dst = select_by_m(R, pascal);
+    emit(R, S, kLArrival, dst, idx);
+    int4 sp = R.spec[idx];
+    bool high;
+    if (sp.w) {  // kv_preloaded: prompt KV starts on the CPU
+        unsigned m = 0;
+        m = m_set_loc(m, LOC_CPU);
+        m = m_set_phase(m, sp.y > 0 ? PH_REASON : PH_ANSWER);
+        if (lane_id() == 0) {
+            int4 h = R.hot[idx];
+            h.x = sp.x;
+            R.hot[idx] = h;
+            R.meta[idx] = m;
+            R.rec[idx].prefill_complete = S.now;
+            if (sp.y == 0) R.rec[idx].reasoning_end = S.now;
+        }
+        add_cpu(R, dst, sp.x);
+        high = sp.y > 0 ? true : !pascal;
+    } else {
+        if (lane_id() == 0) R.meta[idx] = m_set_phase(0u, PH_WAIT);
+        high = true;
+    }
+    __syncwarp();
+    enqueue(R, S, dst, idx, high);
+    maybe_start(R, S, dst);
+}
+
+// engine.cpp:285-308
+DEVI void on_prefill_complete(const Rep& R, Scal& S, int idx) {
+    unsigned m = R.meta[idx];
+    int i = m_owner(m);
+    int4 sp = R.spec[idx];
+    if (lane_id() == 0) R.s.busy[i] = 0;
+    int kv = sp.x + (sp.y == 0 ? 1 : 0);
+    double iter_start = R.s.iter_start[i];
+    __syncwarp();
+    if (lane_id() == 0) {
+        int4 h = R.hot[idx];
+        h.x = kv;
+        if (sp.y == 0) h.y = 1;
+        R.hot[idx] = h;
+        R.rec[idx].prefill_complete = S.now;
+    }
+    __syncwarp();
+    emit(R, S, kLPrefillComplete, i, idx);
+    S.req_iters++;
+    if (sp.y == 0) {
+        if (lane_id() == 0) {
+            R.rec[idx].reasoning_end = S.now;
+            deliver_lane(R, S.now, idx, iter_start);
+        }
+        S.ans_tokens++;
+        __syncwarp();
+        if (1 == sp.z) {
+            // phase = Answering; finish_request (engine.cpp:135-146)
+            int4 h = R.hot[idx];
+            if (lane_id() == 0) {
+                dequeue_lane(R, idx, i, m, h.w);
+                R.meta[idx] = m_set_phase(m, PH_DONE);
+                R.rec[idx].completion = S.now;
+            }
+            // free_memory: waiting-prefill requests default to Gpu
+            add_gpu(R, S, i, -(long long)kv);
+            S.done++;
+            __syncwarp();
+            emit(R, S, kLFinish, i, idx);
+        } else {
+            if (lane_id() == 0) R.meta[idx] = m_set_phase(m, PH_ANSWER);
+            __syncwarp();
+            emit(R, S, kLTransition, i, idx);
+            if (R.policy == kPascal) pascal_transition(R, S, idx);
+        }
+    } else {
+        if (lane_id() == 0) R.meta[idx] = m_set_phase(m, PH_REASON);
+        __syncwarp();
+    }
+    maybe_start(R, S, i);
+}
+
+// engine.cpp:310-337: retire one decode iteration, batch members in plan order.
+DEVI void on_iteration_complete(const Rep& R, Scal& S, int i) {
+    if (lane_id() == 0) R.s.busy[i] = 0;
+    int nb = R.s.blen[i];
+    double iter_start = R.s.iter_start[i];
+    __syncwarp();
+    if (lane_id() == 0) R.s.blen[i] = 0;
+    const bool use_quanta = R.policy == kRr || R.policy == kPascal;
+    const bool pascal = R.policy == kPascal;
+    const unsigned* bin = R.batch + (long long)i * R.n;
+    S.req_iters += nb;
+    for (int base = 0; base < nb; base += 32) {
+        int k = base + lane_id();
+        bool act = k < nb;
+        int idx = 0;
+        int4 h = make_int4(0, 0, 0, 0), sp = make_int4(0, 0, 0, 0);
+        unsigned m = 0;
+        int qu = 0;
+        bool fresh_lost = false;
+        if (act) {
+            idx = (int)bin[k];
+            h = R.hot[idx];
+            m = R.meta[idx];
+            sp = R.spec[idx];
+            h.y += 1;
+            h.x += 1;
+            if (use_quanta) {
+                qu = R.qused[idx] + 1;
+                if ((long long)qu >= R.quantum) {
+                    qu = 0;
+                    h.w += 1;
+                    // a_i counts low-queue members with no exhausted quantum
+                    fresh_lost = m_qlow(m) && h.z != 0 && h.w == 1;
+                }
+            }
+        }
+        const unsigned ph = m_phase(m);
+        const bool trans = act && ph == PH_REASON && h.y == sp.y;
+        const bool ans = act && ph == PH_ANSWER;
+        const bool fin = ans && h.y == sp.y + sp.z;
+        S.ans_tokens += __popc(__ballot_sync(FULL, ans));
+        unsigned remaining = __ballot_sync(FULL, act);
+        unsigned tmask = pascal ? __ballot_sync(FULL, trans) : 0u;
+        while (remaining) {
+            int t = tmask ? __ffs(tmask) - 1 : 32;
+            unsigned seg = remaining & (t == 32 ? FULL : ((1u << t) - 1u));
+            bool in = (seg >> lane_id()) & 1u;
+            // ---- parallel segment: token, quanta, delivery, finish
+            int lines = in ? 1 + (fin ? 1 : 0) + ((!pascal && trans) ? 1 : 0) : 0;
+            int ltot;
+            int lpos = warp_excl_scan(lines, &ltot);
+            long long freed = 0;
+            if (in) {
+                unsigned mm = m;
+                log_put(R, S.nlog + lpos, S.now, kLToken, i, idx, 0);
+                if (trans) {  // baselines: phase flips, placement kept (engine.cpp:164)
+                    mm = m_set_phase(mm, PH_ANSWER);
+                    R.rec[idx].reasoning_end = S.now;
+                    log_put(R, S.nlog + lpos + 1, S.now, kLTransition, i, idx, 0);
+                }
+                if (ans) deliver_lane(R, S.now, idx, iter_start);
+                int4 hw = h;
+                if (fin) {
+                    // finish_request: free GPU KV, dequeue, record completion
+                    freed = h.x;
+                    hw.z = 0;
+                    if (m_qlow(m)) {
+                        atomicSub(&R.s.lcount[i], 1);
+                        if (h.w == 0) atomicSub(&R.s.afresh[i], 1);
+                    } else {
+                        atomicSub(&R.s.hcount[i], 1);
+                    }
+                    mm = m_set_phase(mm, PH_DONE);
+                    R.rec[idx].completion = S.now;
+                    log_put(R, S.nlog + lpos + 1, S.now, kLFinish, i, idx, 0);
+                }
+                if (fresh_lost) atomicSub(&R.s.afresh[i], 1);
+                R.hot[idx] = hw;
+                if (use_quanta) R.qused[idx] = qu;
+                if (mm != m) R.meta[idx] = mm;
+            }
+            S.nlog += ltot;
+            long long fr = warp_sum_ll(freed);
+            if (fr) add_gpu(R, S, i, -fr);
+            S.done += __popc(__ballot_sync(FULL, in && fin));
+            __syncwarp();
+            if (t == 32) break;
+            // ---- Pascal phase boundary for lane t, applied in batch order
+            int tidx = __shfl_sync(FULL, idx, t);
+            if (lane_id() == t) {
+                R.hot[idx] = h;
+                if (use_quanta) R.qused[idx] = qu;
+                if (fresh_lost) atomicSub(&R.s.afresh[i], 1);
+                R.meta[idx] = m_set_phase(m, PH_ANSWER);
+                R.rec[idx].reasoning_end = S.now;
+            }
+            __syncwarp();
+            emit(R, S, kLToken, i, tidx);
+            emit(R, S, kLTransition, i, tidx);
+            pascal_transition(R, S, tidx);
+            remaining &= ~((2u << t) - 1u);
+            tmask &= ~(1u << t);
+        }
+    }
+    __syncwarp();
+    maybe_start(R, S, i);
+}
+
+// engine.cpp:339-349
+DEVI void on_swap_complete(const Rep& R, Scal& S, int idx) {
+    unsigned m = R.meta[idx];
+    int i = m_owner(m);
+    if (lane_id() == 0) {
+        unsigned mm = m;
+        if (m_swout(m)) mm = m_set_swout(mm, false);
+        else if (m_swin(m)) mm = m_set_loc(m_set_swin(mm, false), LOC_GPU);
+        R.meta[idx] = mm;
+    }
+    __syncwarp();
+    emit(R, S, kLSwapComplete, i, idx);
+    maybe_start(R, S, i);
+}
+
+// engine.cpp:351-367
+DEVI void on_transfer_complete(const Rep& R, Scal& S, int idx) {
+    unsigned m = R.meta[idx];
+    int dst = m_owner(m);
+    long long kv = R.hot[idx].x;
+    bool fits = R.cap - R.s.gpu[dst] >= kv;
+    if (fits) add_gpu(R, S, dst, kv);
+    else add_cpu(R, dst, kv);
+    if (lane_id() == 0) {
+        R.meta[idx] = m_set_loc(m, fits ? LOC_GPU : LOC_CPU);
+        R.qused[idx] = 0;
+        int4 h = R.hot[idx];
+        h.w = 0;
+        R.hot[idx] = h;
+    }
+    __syncwarp();
+    enqueue(R, S, dst, idx, false);
+    emit(R, S, kLTransferComplete, dst, idx);
+    note_peak(S);
+    maybe_start(R, S, dst);
+}
+
+// ------------------------------------------------------------ the replica
+DEVI void run_replica(const Arena& a, int r, char* smem) {
+    const ReplicaDesc d = a.desc[r];
+    Rep R;
+    R.n = d.n;
+    R.ni = d.ni;
+    R.policy = d.policy;
+    R.flags = d.flags;
+    R.cap = d.capacity;
+    R.quantum = d.quantum;
+    R.demotion = d.demotion;
+    R.slack = d.slack;
+    R.tpot = d.tpot;
+    R.prof = d.prof;
+    R.logcap = d.log_cap;
+    const long long g = d.req_base;
+    R.arrival = a.arrival + g;
+    R.spec = a.spec + g;
+    R.aoff = a.aoff + g;
+    R.hot = a.hot + g;
+    R.meta = a.meta + g;
+    R.qused = a.qused + g;
+    R.ndel = a.ndel + g;
+    R.cursor = a.cursor + g;
+    R.rec = a.rec + g;
+    R.dig = a.dig;
+    R.del = a.del;
+    R.qent = a.qent + d.queue_base;
+    R.qcap = d.qcap;
+    R.batch = a.batch + d.batch_base;
+    R.heap = a.heap + d.heap_base;
+    R.cand = a.cand + g;
+    R.tmp = a.tmp + g;
+    R.tmpq = a.tmpq + g;
+    R.cstat = a.cstat + g;
+    R.elist = a.elist + g;
+    R.stack = a.stack + g;
+    R.log = a.log + d.log_base;
+    const int ni = d.ni;
+    R.s.gpu = reinterpret_cast<long long*>(smem);
+    R.s.cpu = R.s.gpu + ni;
+    R.s.iter_start = reinterpret_cast<double*>(R.s.cpu + ni);
+    R.s.link = R.s.iter_start + ni;
+    R.s.hi_len = reinterpret_cast<int*>(R.s.link + ni);
+    R.s.lo_len = R.s.hi_len + ni;
+    R.s.hcount = R.s.lo_len + ni;
+    R.s.lcount = R.s.hcount + ni;
+    R.s.afresh = R.s.lcount + ni;
+    R.s.blen = R.s.afresh + ni;
+    R.s.busy = R.s.blen + ni;
+    R.s.healthy = R.s.busy + ni;
+    for (int i = lane_id(); i < ni; i += 32) {
+        R.s.gpu[i] = 0;
+        R.s.cpu[i] = 0;
+        R.s.iter_start[i] = 0.0;
+        R.s.link[i] = 0.0;
+        R.s.hi_len[i] = R.s.lo_len[i] = R.s.hcount[i] = R.s.lcount[i] = 0;
+        R.s.afresh[i] = R.s.blen[i] = R.s.busy[i] = 0;
+        R.s.healthy[i] = 1;
+    }
+    // reset per-request state (Simulator::run, engine.cpp:382-389)
+    for (int k = lane_id(); k < R.n; k += 32) {
+        R.hot[k] = make_int4(0, 0, 0, 0);
+        R.meta[k] = m_set_phase(0u, PH_WAIT);
+        R.qused[k] = 0;
+        R.ndel[k] = 0;
+        R.cursor[k] = 0;
+        RecOut z;
+        z.arrival = z.prefill_complete = z.reasoning_end = z.first_answer_delivery = 0.0;
+        z.first_answer_iter_start = z.blocked = z.completion = z.mig_start = z.mig_end = 0.0;
+        z.nmig = 0;
+        z.pad = 0;
+        R.rec[k] = z;
+    }
+    __syncwarp();
+
+    Scal S;
+    S.now = 0.0;
+    S.evseq = (unsigned long long)R.n;  // arrivals hold seqs 1..n (engine.cpp:384-389)
+    S.enq = 0;
+    S.next_arr = 0;
+    S.hn = 0;
+    S.done = 0;
+    S.status = 0;
+    S.gpu_total = 0;
+    S.peak = 0;
+    S.nlog = 0;
+    S.events = S.plans = S.visits = S.req_iters = S.ans_tokens = S.health = 0;
+    const long long heap_cap = (long long)R.n + R.ni + 1;
+
+    while (S.status == 0) {
+        const bool has_arr = S.next_arr < R.n;
+        const bool has_ev = S.hn > 0;
+        if (!has_arr && !has_ev) break;
+        double ta = has_arr ? R.arrival[S.next_arr] : 0.0;
+        HeapEnt top;
+        top.t = 0.0;
+        top.key = 0;
+        if (has_ev) top = R.heap[1];
+        // arrivals carry seqs 1..n, below every dynamic event seq
+        bool take_arr = has_arr && (!has_ev || !(top.t < ta));
+        double et;
+        unsigned kind, id;
+        if (take_arr) {
+            et = ta;
+            kind = 0;
+            id = (unsigned)S.next_arr++;
+        } else {
+            HeapEnt e = heap_pop(R, S);
+            et = e.t;
+            kind = (unsigned)(e.key >> 26) & 7u;
+            id = (unsigned)(e.key & ((1u << 26) - 1u));
+        }
+        S.events++;
+        if (et < S.now - 1e-12) {
+            S.status = kErrClock;
+            break;
+        }
+        S.now = dmax(S.now, et);
+        switch (kind) {
+            case 0: on_arrival(R, S, (int)id); break;
+            case EV_PREFILL: on_prefill_complete(R, S, (int)id); break;
+            case EV_ITER: on_iteration_complete(R, S, (int)id); break;
+            case EV_SWAP: on_swap_complete(R, S, (int)id); break;
+            case EV_TRANSFER: on_transfer_complete(R, S, (int)id); break;
+        }
+        if (S.hn + 1 > heap_cap && S.status == 0) S.status = kErrHeap;
+    }
+    if (S.status == 0 && S.done != R.n) S.status = kErrStall;
+    if (lane_id() == 0) {
+        ReplicaOut o;
+        o.status = S.status;
+        o.pad = 0;
+        o.peak = S.peak;
+        o.nlog = S.nlog;
+        o.events = S.events;
+        o.plans = S.plans;
+        o.visits = S.visits;
+        o.req_iters = S.req_iters;
+        o.answer_tokens = S.ans_tokens;
+        o.health_checks = S.health;
+        o.now = S.now;
+        a.out[r] = o;
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(128) sched_kernel(Arena a, int max_ni) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int warp = threadIdx.x >> 5;
+    char* smem = smem_raw + warp * smem_per_warp(max_ni);
+    while (true) {
+        int r = 0;
+        if (lane_id() == 0) r = atomicAdd(a.work, 1);
+        r = __shfl_sync(FULL, r, 0);
+        if (r >= a.n_rep) break;
+        run_replica(a, r, smem);
+    }
+}
+
+int launch_engine(const Arena& a, int max_ni, int warps_per_block, int blocks, void* stream) {
+    if (warps_per_block < 1 || warps_per_block > 4) return 1;
+    size_t smem = (size_t)warps_per_block * smem_per_warp(max_ni);
+    if (smem > 48 * 1024) {
+        if (cudaFuncSetAttribute(sched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+            return 2;
+    }
+    sched_kernel<<<blocks, warps_per_block * 32, smem, (cudaStream_t)stream>>>(a, max_ni);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+}  // namespace pb

@@ -1,0 +1,187 @@
+// engine.h — layout shared by the host driver (engine_host.cpp) and the
+// sm_100a scheduling engine (engine.cu).
+//
+// One warp simulates one replica (one trace under one policy/config) end to
+// end: the reference's serial (time, seq) event chain (proj/src/engine.cpp:
+// 392-404) stays serial, and each handler's inner loops (queue scans, priority
+// partition, admission, plan application, batch retire, monitor snapshots)
+// run across the 32 lanes. Many replicas run side by side, one per warp, so a
+// replica sweep fills all 148 SMs.
+//
+// All per-request state is struct-of-arrays in HBM, indexed by
+// g = ReplicaDesc::req_base + i (i = trace index). Per-instance state lives in
+// shared memory for the lifetime of the replica.
+#pragma once
+
+#include <cstdint>
+
+#include <vector_types.h>  // int4 / uint2 (CUDA vector types, host and device)
+
+namespace pb {
+
+enum Policy : int { kFcfs = 0, kRr = 1, kOracle = 2, kPascal = 3 };
+
+// ReplicaDesc::flags
+enum : int {
+    kNoMigration = 1,   // Ablations::no_migration (proj/include/pascalsim/cluster.hpp:13-16)
+    kNonAdaptive = 2,   // Ablations::non_adaptive
+    kRecordDeliv = 4,   // keep every answer delivery time (records / parity mode)
+    kLogEvents = 8,     // write the decision log (pascal-events-v1 entries)
+};
+
+// proj/include/pascalsim/costmodel.hpp:12-21
+struct Profile {
+    double prefill_base, prefill_per_token;
+    double decode_base, decode_per_request, decode_per_kv_token;
+    double swap_bandwidth, fabric_bandwidth, fabric_latency;
+};
+
+struct ReplicaDesc {
+    int n;        // requests
+    int ni;       // instances
+    int policy;
+    int flags;
+    long long capacity;  // per-instance KV capacity (tokens)
+    long long quantum, demotion, slack;
+    double tpot;
+    Profile prof;
+    long long req_base;    // into request arrays
+    long long ans_base;    // into digest/delivery arenas (unused: aoff is absolute)
+    long long queue_base;  // into qent: 2 queues per instance, qcap entries each
+    long long qcap;
+    long long batch_base;  // into batch: ni * n entries
+    long long heap_base;   // into heap: n + ni + 2 entries
+    long long log_base, log_cap;
+};
+
+// Counters the device reports per replica (roofline accounting).
+struct ReplicaOut {
+    int status;      // 0 ok, else kErr*
+    int pad;
+    long long peak;  // peak sum of gpu_used (engine.cpp:75-79)
+    long long nlog;  // log entries produced (may exceed log_cap)
+    long long events, plans, visits, req_iters, answer_tokens, health_checks;
+    double now;      // clock at the end of the run
+};
+
+enum : int {
+    kErrNone = 0,
+    kErrPast = 1,      // "event scheduled in the past"      engine.cpp:86-87
+    kErrClock = 2,     // "clock moved backwards"            engine.cpp:395
+    kErrCapacity = 3,  // "instance over GPU capacity"       engine.cpp:255-256
+    kErrStall = 4,     // "simulation stalled with unfinished requests"  :424
+    kErrHeap = 5,      // device heap overflow (internal)
+};
+
+// Per-request record, proj/include/pascalsim/metrics.hpp:15-28 (vectors live
+// in the digest/delivery arenas; at most one migration per request).
+struct RecOut {
+    double arrival, prefill_complete, reasoning_end, first_answer_delivery,
+        first_answer_iter_start, blocked, completion, mig_start, mig_end;
+    int nmig, pad;
+};
+
+struct HeapEnt {
+    double t;
+    unsigned long long key;  // seq(35) | kind(3) | id(26)
+};
+
+struct LogEnt {
+    double t;
+    int req;  // trace index or -1
+    int inst;
+    int kind;
+    int detail;
+};
+
+enum LogKind : int {
+    kLArrival = 0, kLDemote, kLEvict, kLSwapIn, kLBlock, kLPrefillStart, kLDecodeStart,
+    kLPrefillComplete, kLToken, kLTransition, kLMigrate, kLFinish, kLSwapComplete,
+    kLTransferComplete
+};
+
+// Batch-wide device arenas.
+struct Arena {
+    const ReplicaDesc* desc;
+    ReplicaOut* out;
+    int n_rep;
+    int* work;  // work-stealing counter
+    // read-only trace
+    const double* arrival;
+    const int4* spec;       // {prompt, reasoning, answering, kv_preloaded}
+    const long long* aoff;  // absolute offset of the request's answer slots
+    // mutable request state
+    int4* hot;        // {kv, tokens, enqueue_seq (0 = not queued), quanta_exhausted}
+    unsigned* meta;   // phase:2 | loc:2 | swin:1 | swout:1 | qlow:1 | owner:16 (<<8)
+    int* qused;       // quantum_used_in_round
+    int* ndel;        // delivered answer tokens
+    int* cursor;      // digests known <= a past `now` (pacer health cursor)
+    RecOut* rec;
+    double* dig;      // digest times (always)
+    double* del;      // delivery times (kRecordDeliv)
+    // queues / batches / events
+    uint2* qent;      // {request index, enqueue_seq}
+    unsigned* batch;
+    HeapEnt* heap;
+    // per-replica scratch, n entries each (indexed by req_base)
+    int4* cand;
+    int4* tmp;
+    unsigned* tmpq;
+    unsigned char* cstat;
+    unsigned* elist;
+    unsigned* stack;
+    LogEnt* log;
+};
+
+// Per-replica metric parameters (RunConfig fields used by build_report).
+struct MetricParams {
+    double tpot, qoe_threshold, ttfat_target;
+    long long req_base;
+    int n;
+    int pad;
+};
+
+// Device-computed build_report aggregates + counters; same layout as
+// pascal_summary in include/pascal_b200.h.
+struct DevSummary {
+    double ttft_mean, ttft_p50, ttft_p90, ttft_p95, ttft_p99;
+    double slo_rate, ttfat_attain, throughput;
+    long long capacity, requests, req_iters, answer_tokens, events, plans, visits, health;
+    long long slo_violations;
+    int status, pad;
+};
+
+// Per-request metric outputs (trace order), proj/include/pascalsim/metrics.hpp:58-67.
+struct RowArrays {
+    double* ttft;
+    double* ttfat;
+    double* qoe;
+    double* blocking;
+    unsigned char* slo;
+    double* ttft_sorted;
+};
+
+#ifdef __CUDACC__
+#define PB_HD __host__ __device__
+#else
+#define PB_HD
+#endif
+
+// Dynamic shared memory per warp for ni instances.
+PB_HD inline int smem_per_warp(int ni) { return ni * 64 + 16; }
+
+// Host entries (engine.cu / metrics.cu). All enqueue on `stream`.
+int launch_engine(const Arena& a, int max_ni, int warps_per_block, int blocks,
+                  void* stream);
+// capacity = max(ceil(fraction * peak / ni), biggest) for the replicas listed
+// in `map` (derive_capacity, proj/src/engine.cpp:466-470); writes echo[r] and,
+// unless the replica runs the oracle policy, desc[r].capacity.
+int launch_capacity(ReplicaDesc* desc, const ReplicaOut* oracle_out, const int* map,
+                    const double* fraction, const long long* biggest, long long* echo,
+                    int count, void* stream);
+int launch_metrics(const Arena& a, const MetricParams* params, const long long* seg,
+                   const int* rid, long long total, int n_rep, RowArrays rows,
+                   DevSummary* out, const long long* echo_capacity, void* sort_tmp,
+                   size_t* sort_tmp_bytes, void* stream);
+
+}  // namespace pb

@@ -1,0 +1,538 @@
+// engine_host.cpp — host driver of the device scheduling engine.
+//
+// Packs traces into the struct-of-arrays layout of engine.h, owns the device
+// arenas, launches (1) the oracle pre-run for capacity derivation
+// (proj/src/engine.cpp:449-471), (2) the capacity kernel, (3) the policy run,
+// (4) the metric kernels — all on one stream with no host round trip in
+// between — and fetches summaries, per-request rows, records and the decision
+// log. There is no CPU execution path: without a CUDA device every run fails
+// with PASCAL_ERR_INTERNAL.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <memory>
+#include <numeric>
+
+#include "common.hpp"
+
+namespace pbh {
+
+namespace {
+
+thread_local Timing g_timing;
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw std::logic_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void ensure(size_t count) {
+        if (count <= n && p) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        size_t c = std::max<size_t>(count, 1);
+        ck(cudaMalloc(&p, c * sizeof(T)), "cudaMalloc");
+        n = c;
+    }
+};
+
+constexpr int kWarpsPerBlock = 4;
+constexpr long long kMaxReq = (1ll << 26) - 1;  // heap id field
+constexpr int kMaxInst = 512;
+
+int sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+void check_limits(const Job& j) {
+    const RunCfg& c = j.cfg;
+    if (c.instances < 1) throw std::invalid_argument("instance_count must be >= 1");
+    if (c.instances > kMaxInst)
+        throw std::invalid_argument("instance_count exceeds the device engine limit (512)");
+    if ((long long)j.trace->size() > kMaxReq)
+        throw std::invalid_argument("trace exceeds the device engine limit (2^26-1 requests)");
+    if (!(c.tpot > 0.0)) throw std::invalid_argument("target_tpot must be > 0");
+    for (const Spec& s : *j.trace)
+        if (s.max_kv() > (long)INT_MAX / 2)
+            throw std::invalid_argument("request KV footprint exceeds the device engine limit");
+}
+
+}  // namespace
+
+Timing& last_timing() { return g_timing; }
+
+bool device_available() {
+    int n = 0;
+    return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+}
+
+void set_device(int dev) { ck(cudaSetDevice(dev), "cudaSetDevice"); }
+
+const char* status_message(int st) {
+    switch (st) {
+        case pb::kErrPast: return "event scheduled in the past";
+        case pb::kErrClock: return "clock moved backwards";
+        case pb::kErrCapacity: return "instance over GPU capacity";
+        case pb::kErrStall: return "simulation stalled with unfinished requests";
+        case pb::kErrHeap: return "device event heap overflow";
+        default: return "ok";
+    }
+}
+
+// ------------------------------------------------------------------ Batch
+class Batch {
+public:
+    explicit Batch(const std::vector<Job>& jobs);
+    ~Batch();
+    void execute();
+    void fetch_summaries(std::vector<DeviceSummary>& out);
+    void fetch_single(RunOutputs& o, bool records, bool log);
+    void enable_log(long long cap) { log_cap_ = cap; }
+    void enable_records() { records_ = true; }
+    void build();
+
+    std::vector<Job> jobs_;
+    bool records_ = false;
+    long long log_cap_ = 0;
+    bool built_ = false;
+
+    int n_rep_ = 0, max_ni_ = 1;
+    long long total_req_ = 0, total_ans_ = 0, total_q_ = 0, total_batch_ = 0, total_heap_ = 0,
+              total_log_ = 0;
+    std::vector<pb::ReplicaDesc> desc_;
+    std::vector<pb::ReplicaDesc> odesc_;  // oracle pre-run descriptors
+    std::vector<int> omap_;
+    std::vector<long long> echo_static_;
+
+    cudaStream_t st_ = nullptr;
+    cudaEvent_t ev_[5] = {};
+    DevBuf<pb::ReplicaDesc> d_desc_, d_odesc_, d_desc_init_;
+    DevBuf<pb::ReplicaOut> d_out_, d_oout_;
+    DevBuf<int> d_work_, d_omap_, d_rid_;
+    DevBuf<double> d_arrival_, d_frac_;
+    DevBuf<int4> d_spec_, d_hot_, d_cand_, d_tmp_;
+    DevBuf<long long> d_aoff_, d_biggest_, d_echo_, d_seg_;
+    DevBuf<unsigned> d_meta_, d_batch_, d_tmpq_, d_elist_, d_stack_;
+    DevBuf<int> d_qused_, d_ndel_, d_cursor_;
+    DevBuf<pb::RecOut> d_rec_;
+    DevBuf<double> d_dig_, d_del_;
+    DevBuf<uint2> d_qent_;
+    DevBuf<pb::HeapEnt> d_heap_;
+    DevBuf<unsigned char> d_cstat_, d_slo_;
+    DevBuf<pb::LogEnt> d_log_;
+    DevBuf<pb::MetricParams> d_params_;
+    DevBuf<double> d_ttft_, d_ttfat_, d_qoe_, d_block_, d_sorted_;
+    DevBuf<pb::DevSummary> d_sum_;
+    DevBuf<char> d_sort_tmp_;
+    size_t sort_bytes_ = 0;
+
+    pb::Arena arena(bool oracle) const;
+};
+
+Batch::Batch(const std::vector<Job>& jobs) : jobs_(jobs) {
+    for (const Job& j : jobs_) {
+        check_trace(*j.trace);
+        check_profile(j.prof);
+        check_limits(j);
+    }
+}
+
+Batch::~Batch() {
+    for (auto& e : ev_)
+        if (e) cudaEventDestroy(e);
+    if (st_) cudaStreamDestroy(st_);
+}
+
+void Batch::build() {
+    if (built_) return;
+    built_ = true;
+    n_rep_ = (int)jobs_.size();
+    ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+    for (auto& e : ev_) ck(cudaEventCreate(&e), "event");
+    Timing& tm = g_timing;
+    tm = Timing{};
+
+    // ---- layout
+    desc_.resize(n_rep_);
+    std::vector<pb::MetricParams> params(n_rep_);
+    std::vector<double> frac(n_rep_);
+    std::vector<long long> biggest(n_rep_), seg(n_rep_ + 1);
+    echo_static_.assign(n_rep_, 0);
+    odesc_.clear();
+    omap_.clear();
+    long long rq = 0, ans = 0, q = 0, bt = 0, hp = 0, lg = 0;
+    for (int r = 0; r < n_rep_; ++r) {
+        const Job& j = jobs_[r];
+        const long long n = (long long)j.trace->size();
+        const int ni = j.cfg.instances;
+        pb::ReplicaDesc d{};
+        d.n = (int)n;
+        d.ni = ni;
+        d.policy = j.cfg.policy;
+        d.flags = (j.cfg.no_migration ? pb::kNoMigration : 0) |
+                  (j.cfg.non_adaptive ? pb::kNonAdaptive : 0) |
+                  (records_ ? pb::kRecordDeliv : 0) | (log_cap_ > 0 ? pb::kLogEvents : 0);
+        d.quantum = j.cfg.quantum;
+        d.demotion = j.cfg.demotion;
+        d.slack = j.cfg.slack;
+        d.tpot = j.cfg.tpot;
+        d.prof = j.prof;
+        d.req_base = rq;
+        d.ans_base = ans;
+        d.qcap = n + 1;
+        d.queue_base = q;
+        d.batch_base = bt;
+        d.heap_base = hp;
+        d.log_base = lg;
+        d.log_cap = log_cap_;
+        long long big = 0;
+        for (const Spec& s : *j.trace) big = std::max(big, (long long)s.max_kv());
+        biggest[r] = big;
+        frac[r] = j.cfg.capacity_fraction;
+        const long long kOracleCap = LONG_MAX / 4;
+        if (j.cfg.gpu_capacity > 0) {
+            echo_static_[r] = std::max<long long>(j.cfg.gpu_capacity, big);
+            d.capacity = j.cfg.policy == pb::kOracle ? kOracleCap : echo_static_[r];
+        } else {
+            d.capacity = kOracleCap;  // overwritten by the capacity kernel unless oracle
+            pb::ReplicaDesc od = d;
+            od.policy = pb::kOracle;
+            od.flags = 0;
+            od.capacity = kOracleCap;
+            od.log_cap = 0;
+            odesc_.push_back(od);
+            omap_.push_back(r);
+        }
+        desc_[r] = d;
+        params[r] = pb::MetricParams{j.cfg.tpot, j.cfg.qoe_threshold, j.cfg.ttfat_target, rq,
+                                     (int)n, 0};
+        seg[r] = rq;
+        max_ni_ = std::max(max_ni_, ni);
+        rq += n;
+        for (const Spec& s : *j.trace) ans += s.answering;
+        q += 2ll * ni * (n + 1);
+        bt += (long long)ni * std::max<long long>(n, 1);
+        hp += n + ni + 2;
+        lg += log_cap_;
+    }
+    seg[n_rep_] = rq;
+    total_req_ = rq;
+    total_ans_ = ans;
+    total_q_ = q;
+    total_batch_ = bt;
+    total_heap_ = hp;
+    total_log_ = lg;
+
+    // ---- host staging of the read-only trace
+    std::vector<double> arrival(rq);
+    std::vector<int4> spec(rq);
+    std::vector<long long> aoff(rq);
+    std::vector<int> rid(rq);
+    long long g = 0, a = 0;
+    for (int r = 0; r < n_rep_; ++r)
+        for (const Spec& s : *jobs_[r].trace) {
+            arrival[g] = s.arrival;
+            spec[g] = make_int4((int)s.prompt, (int)s.reasoning, (int)s.answering, s.preloaded ? 1 : 0);
+            aoff[g] = a;
+            rid[g] = r;
+            a += s.answering;
+            ++g;
+        }
+
+    // ---- device arenas
+    d_desc_.ensure(n_rep_);
+    d_desc_init_.ensure(n_rep_);
+    d_out_.ensure(n_rep_);
+    d_odesc_.ensure(odesc_.size());
+    d_oout_.ensure(odesc_.size());
+    d_omap_.ensure(omap_.size());
+    d_work_.ensure(2);
+    d_arrival_.ensure(rq);
+    d_spec_.ensure(rq);
+    d_aoff_.ensure(rq);
+    d_rid_.ensure(rq);
+    d_hot_.ensure(rq);
+    d_meta_.ensure(rq);
+    d_qused_.ensure(rq);
+    d_ndel_.ensure(rq);
+    d_cursor_.ensure(rq);
+    d_rec_.ensure(rq);
+    d_cand_.ensure(rq);
+    d_tmp_.ensure(rq);
+    d_tmpq_.ensure(rq);
+    d_cstat_.ensure(rq);
+    d_elist_.ensure(rq);
+    d_stack_.ensure(rq);
+    d_dig_.ensure(ans);
+    d_del_.ensure(records_ ? ans : 1);
+    d_qent_.ensure(q);
+    d_batch_.ensure(bt);
+    d_heap_.ensure(hp);
+    d_log_.ensure(std::max<long long>(lg, 1));
+    d_params_.ensure(n_rep_);
+    d_frac_.ensure(n_rep_);
+    d_biggest_.ensure(n_rep_);
+    d_echo_.ensure(n_rep_);
+    d_seg_.ensure(n_rep_ + 1);
+    d_ttft_.ensure(rq);
+    d_ttfat_.ensure(rq);
+    d_qoe_.ensure(rq);
+    d_block_.ensure(rq);
+    d_slo_.ensure(rq);
+    d_sorted_.ensure(rq);
+    d_sum_.ensure(n_rep_);
+
+    pb::RowArrays rows{d_ttft_.p, d_ttfat_.p, d_qoe_.p, d_block_.p, d_slo_.p, d_sorted_.p};
+    pb::Arena ar = arena(false);
+    size_t bytes = 0;
+    if (pb::launch_metrics(ar, d_params_.p, d_seg_.p, d_rid_.p, rq, n_rep_, rows, d_sum_.p,
+                           d_echo_.p, nullptr, &bytes, st_) != 0)
+        throw std::logic_error("CUB size query failed");
+    sort_bytes_ = std::max<size_t>(bytes, 16);
+    d_sort_tmp_.ensure(sort_bytes_);
+
+    // ---- uploads (timed as h2d)
+    ck(cudaEventRecord(ev_[0], st_), "event");
+    long long hb = 0;
+    auto up = [&](void* dst, const void* src, size_t b) {
+        if (b == 0) return;
+        ck(cudaMemcpyAsync(dst, src, b, cudaMemcpyHostToDevice, st_), "h2d");
+        hb += (long long)b;
+    };
+    up(d_desc_init_.p, desc_.data(), desc_.size() * sizeof(pb::ReplicaDesc));
+    up(d_odesc_.p, odesc_.data(), odesc_.size() * sizeof(pb::ReplicaDesc));
+    up(d_omap_.p, omap_.data(), omap_.size() * sizeof(int));
+    up(d_arrival_.p, arrival.data(), arrival.size() * sizeof(double));
+    up(d_spec_.p, spec.data(), spec.size() * sizeof(int4));
+    up(d_aoff_.p, aoff.data(), aoff.size() * sizeof(long long));
+    up(d_rid_.p, rid.data(), rid.size() * sizeof(int));
+    up(d_params_.p, params.data(), params.size() * sizeof(pb::MetricParams));
+    up(d_frac_.p, frac.data(), frac.size() * sizeof(double));
+    up(d_biggest_.p, biggest.data(), biggest.size() * sizeof(long long));
+    up(d_echo_.p, echo_static_.data(), echo_static_.size() * sizeof(long long));
+    up(d_seg_.p, seg.data(), seg.size() * sizeof(long long));
+    ck(cudaEventRecord(ev_[1], st_), "event");
+    ck(cudaEventSynchronize(ev_[1]), "sync");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev_[0], ev_[1]);
+    tm.h2d_ms = ms;
+    tm.h2d_bytes = hb;
+}
+
+pb::Arena Batch::arena(bool oracle) const {
+    pb::Arena a{};
+    a.desc = oracle ? d_odesc_.p : d_desc_.p;
+    a.out = oracle ? d_oout_.p : d_out_.p;
+    a.n_rep = oracle ? (int)odesc_.size() : n_rep_;
+    a.work = d_work_.p + (oracle ? 0 : 1);
+    a.arrival = d_arrival_.p;
+    a.spec = d_spec_.p;
+    a.aoff = d_aoff_.p;
+    a.hot = d_hot_.p;
+    a.meta = d_meta_.p;
+    a.qused = d_qused_.p;
+    a.ndel = d_ndel_.p;
+    a.cursor = d_cursor_.p;
+    a.rec = d_rec_.p;
+    a.dig = d_dig_.p;
+    a.del = d_del_.p;
+    a.qent = d_qent_.p;
+    a.batch = d_batch_.p;
+    a.heap = d_heap_.p;
+    a.cand = d_cand_.p;
+    a.tmp = d_tmp_.p;
+    a.tmpq = d_tmpq_.p;
+    a.cstat = d_cstat_.p;
+    a.elist = d_elist_.p;
+    a.stack = d_stack_.p;
+    a.log = d_log_.p;
+    return a;
+}
+
+void Batch::execute() {
+    build();
+    Timing& tm = g_timing;
+    const int sms = sm_count();
+    auto blocks_for = [&](int reps) {
+        int want = (reps + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        return std::max(1, std::min(want, sms * 8));
+    };
+    int launches = 0;
+    ck(cudaEventRecord(ev_[0], st_), "event");
+    ck(cudaMemcpyAsync(d_desc_.p, d_desc_init_.p, n_rep_ * sizeof(pb::ReplicaDesc),
+                       cudaMemcpyDeviceToDevice, st_),
+       "desc reset");
+    ck(cudaMemsetAsync(d_work_.p, 0, 2 * sizeof(int), st_), "memset");
+    if (!odesc_.empty()) {
+        pb::Arena oa = arena(true);
+        if (pb::launch_engine(oa, max_ni_, kWarpsPerBlock, blocks_for((int)odesc_.size()), st_))
+            throw std::logic_error("engine launch failed (oracle pre-run)");
+        if (pb::launch_capacity(d_desc_.p, d_oout_.p, d_omap_.p, d_frac_.p, d_biggest_.p,
+                                d_echo_.p, (int)odesc_.size(), st_))
+            throw std::logic_error("capacity kernel launch failed");
+        launches += 2;
+    }
+    ck(cudaEventRecord(ev_[1], st_), "event");
+    pb::Arena pa = arena(false);
+    if (pb::launch_engine(pa, max_ni_, kWarpsPerBlock, blocks_for(n_rep_), st_))
+        throw std::logic_error("engine launch failed");
+    launches += 1;
+    ck(cudaEventRecord(ev_[2], st_), "event");
+    pb::RowArrays rows{d_ttft_.p, d_ttfat_.p, d_qoe_.p, d_block_.p, d_slo_.p, d_sorted_.p};
+    size_t bytes = sort_bytes_;
+    if (pb::launch_metrics(pa, d_params_.p, d_seg_.p, d_rid_.p, total_req_, n_rep_, rows,
+                           d_sum_.p, d_echo_.p, d_sort_tmp_.p, &bytes, st_) != 0)
+        throw std::logic_error("metrics launch failed");
+    launches += total_req_ > 0 ? 3 : 1;
+    ck(cudaEventRecord(ev_[3], st_), "event");
+    ck(cudaEventSynchronize(ev_[3]), "engine sync");
+    ck(cudaGetLastError(), "engine");
+    float a = 0, b = 0, c = 0, t = 0;
+    cudaEventElapsedTime(&a, ev_[0], ev_[1]);
+    cudaEventElapsedTime(&b, ev_[1], ev_[2]);
+    cudaEventElapsedTime(&c, ev_[2], ev_[3]);
+    cudaEventElapsedTime(&t, ev_[0], ev_[3]);
+    tm.derive_ms = a;
+    tm.engine_ms = b;
+    tm.metrics_ms = c;
+    tm.total_ms = t;
+    tm.launches = launches;
+}
+
+void Batch::fetch_summaries(std::vector<DeviceSummary>& out) {
+    static_assert(sizeof(DeviceSummary) == sizeof(pb::DevSummary), "summary layout");
+    out.resize(n_rep_);
+    ck(cudaEventRecord(ev_[0], st_), "event");
+    ck(cudaMemcpyAsync(out.data(), d_sum_.p, n_rep_ * sizeof(pb::DevSummary),
+                       cudaMemcpyDeviceToHost, st_),
+       "d2h");
+    ck(cudaEventRecord(ev_[1], st_), "event");
+    ck(cudaEventSynchronize(ev_[1]), "sync");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev_[0], ev_[1]);
+    g_timing.d2h_ms = ms;
+    g_timing.d2h_bytes = (long long)(n_rep_ * sizeof(pb::DevSummary));
+}
+
+void Batch::fetch_single(RunOutputs& o, bool records, bool log) {
+    std::vector<DeviceSummary> s;
+    fetch_summaries(s);
+    o.summary = s[0];
+    o.status = s[0].status;
+    o.capacity = s[0].capacity;
+    const long long n = total_req_;
+    std::vector<double> ttft(n), ttfat(n), qoe(n), blk(n);
+    std::vector<unsigned char> slo(n);
+    auto down = [&](void* dst, const void* src, size_t b) {
+        if (b) ck(cudaMemcpy(dst, src, b, cudaMemcpyDeviceToHost), "d2h");
+    };
+    down(ttft.data(), d_ttft_.p, n * sizeof(double));
+    down(ttfat.data(), d_ttfat_.p, n * sizeof(double));
+    down(qoe.data(), d_qoe_.p, n * sizeof(double));
+    down(blk.data(), d_block_.p, n * sizeof(double));
+    down(slo.data(), d_slo_.p, n);
+    const Trace& t = *jobs_[0].trace;
+    o.rows.resize(n);
+    for (long long k = 0; k < n; ++k) {
+        Row& w = o.rows[k];
+        w.id = t[k].id;
+        w.reasoning = t[k].reasoning;
+        w.answering = t[k].answering;
+        w.ttft = ttft[k];
+        w.ttfat = ttfat[k];
+        w.qoe = qoe[k];
+        w.slo = slo[k] != 0;
+        w.blocking = blk[k];
+    }
+    if (records) {
+        o.rec.resize(n);
+        down(o.rec.data(), d_rec_.p, n * sizeof(pb::RecOut));
+        o.dig.resize(total_ans_);
+        down(o.dig.data(), d_dig_.p, total_ans_ * sizeof(double));
+        if (records_) {
+            o.del.resize(total_ans_);
+            down(o.del.data(), d_del_.p, total_ans_ * sizeof(double));
+        }
+        o.aoff.resize(n);
+        down(o.aoff.data(), d_aoff_.p, n * sizeof(long long));
+        std::vector<int> nd(n);
+        down(nd.data(), d_ndel_.p, n * sizeof(int));
+        // ndel travels in rec.pad for the dump writer
+        for (long long k = 0; k < n; ++k) o.rec[k].pad = nd[k];
+    }
+    if (log) {
+        pb::ReplicaOut ro;
+        down(&ro, d_out_.p, sizeof ro);
+        long long cnt = std::min<long long>(ro.nlog, log_cap_);
+        o.log.resize(cnt);
+        down(o.log.data(), d_log_.p, cnt * sizeof(pb::LogEnt));
+        if (ro.nlog > log_cap_) o.log.resize(0), o.capacity = -ro.nlog;  // caller retries
+    }
+}
+
+Batch* batch_create(const std::vector<Job>& jobs) {
+    auto* b = new Batch(jobs);
+    try {
+        b->build();
+    } catch (...) {
+        delete b;
+        throw;
+    }
+    return b;
+}
+void batch_execute(Batch* b) { b->execute(); }
+void batch_summaries(Batch* b, std::vector<DeviceSummary>& out) { b->fetch_summaries(out); }
+void batch_free(Batch* b) { delete b; }
+
+RunOutputs run_single(const Job& job, bool want_records, bool want_log) {
+    if (!device_available()) throw std::logic_error("no CUDA device available for the B200 engine");
+    long long cap = want_log ? std::max<long long>(1024, 4 * request_iterations(*job.trace) +
+                                                             16 * (long long)job.trace->size())
+                             : 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        Batch b({job});
+        if (want_records) b.enable_records();
+        if (want_log) b.enable_log(cap);
+        b.execute();
+        RunOutputs o;
+        b.fetch_single(o, want_records, want_log);
+        if (o.status != 0) throw std::logic_error(status_message(o.status));
+        if (want_log && o.capacity < 0) {  // decision log larger than the first guess
+            cap = -o.capacity;
+            continue;
+        }
+        return o;
+    }
+    throw std::logic_error("event log sizing failed");
+}
+
+long long derive_capacity_dev(const Job& job) {
+    if (job.cfg.instances < 1) throw std::invalid_argument("instance_count must be >= 1");
+    long long big = 0;
+    for (const Spec& s : *job.trace) big = std::max(big, (long long)s.max_kv());
+    if (job.cfg.gpu_capacity > 0) return std::max<long long>(job.cfg.gpu_capacity, big);
+    if (!device_available()) throw std::logic_error("no CUDA device available for the B200 engine");
+    Batch b({job});
+    b.execute();
+    std::vector<DeviceSummary> s;
+    b.fetch_summaries(s);
+    return s[0].capacity;
+}
+
+}  // namespace pbh

@@ -1,0 +1,197 @@
+// metrics.cu — latency-model outputs and metric reduction on the device.
+//
+//   rows_kernel     ttft / ttfat / qoe / slo / blocking per request
+//                   (proj/src/metrics.cpp:34-68); one thread per request so the
+//                   QoE areas are summed sequentially in token order, as the
+//                   reference does (:45-49) — bit-exact, never a tree sum.
+//   segmented sort  TTFTs per replica (CUB segmented sort).
+//   summary_kernel  build_report aggregates (:115-153): mean over the sorted
+//                   TTFTs (sequential, sorted order), nearest-rank P50/P90/
+//                   P95/P99 (:24-31), SLO-violation rate, TTFAT attainment,
+//                   throughput (:70-83); one warp per replica.
+//   capacity_kernel derive_capacity's fraction rule (engine.cpp:466-470).
+
+#include <cuda_runtime.h>
+
+#include <cub/device/device_segmented_sort.cuh>
+
+#include "engine.h"
+
+namespace pb {
+
+constexpr unsigned FULLM = 0xffffffffu;
+
+__global__ void capacity_kernel(ReplicaDesc* desc, const ReplicaOut* oout, const int* map,
+                                const double* fraction, const long long* biggest,
+                                long long* echo, int count) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    int r = map[k];
+    double f = fraction[r] > 0.0 ? fraction[r] : 1.0;
+    double q = __ddiv_rn(__dmul_rn(f, (double)oout[k].peak), (double)desc[r].ni);
+    long long cap = (long long)ceil(q);
+    if (cap < biggest[r]) cap = biggest[r];
+    echo[r] = cap;
+    if (desc[r].policy != kOracle) desc[r].capacity = cap;
+}
+
+__global__ void rows_kernel(const int* rid, const MetricParams* params, const int4* spec,
+                            const long long* aoff, const RecOut* rec, const double* dig,
+                            const int* ndel, RowArrays rows, long long total) {
+    long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= total) return;
+    const MetricParams mp = params[rid[g]];
+    const RecOut r = rec[g];
+    const int4 sp = spec[g];
+    // ttft / ttfat (metrics.cpp:34-36)
+    double ttft = __dsub_rn(r.first_answer_delivery, r.arrival);
+    double ttfat = __dsub_rn(r.first_answer_delivery, r.reasoning_end);
+    // qoe (metrics.cpp:38-52)
+    double q = 1.0;
+    int nd = ndel[g];
+    long long n = sp.z;
+    if (n >= 1 && nd > 0) {
+        const double* d = dig + aoff[g];
+        double t0 = r.first_answer_delivery;
+        double horizon = d[nd - 1];
+        if (horizon > t0) {
+            double da = 0.0;
+            for (int k = 0; k < nd; ++k) {
+                double x = __dsub_rn(horizon, d[k]);
+                da = __dadd_rn(da, 0.0 < x ? x : 0.0);
+            }
+            double ea = 0.0;
+            for (long long k = 0; k < n; ++k) {
+                double x = __dsub_rn(horizon, __dadd_rn(t0, __dmul_rn((double)k, mp.tpot)));
+                ea = __dadd_rn(ea, 0.0 < x ? x : 0.0);
+            }
+            if (ea > 0.0) q = __ddiv_rn(da, ea);
+        }
+    }
+    // blocking latency (metrics.cpp:58-68)
+    double lo = r.reasoning_end, hi = r.first_answer_iter_start, mig = 0.0;
+    if (r.nmig) {
+        double a = lo < r.mig_start ? r.mig_start : lo;
+        double b = r.mig_end < hi ? r.mig_end : hi;
+        if (b > a) mig = __dadd_rn(mig, __dsub_rn(b, a));
+    }
+    double blk = __dsub_rn(__dsub_rn(hi, lo), mig);
+    if (!(0.0 < blk)) blk = 0.0;
+    rows.ttft[g] = ttft;
+    rows.ttfat[g] = ttfat;
+    rows.qoe[g] = q;
+    rows.blocking[g] = blk;
+    rows.slo[g] = q < mp.qoe_threshold ? 1 : 0;
+}
+
+__device__ __forceinline__ double nearest_rank(const double* v, long long n, double pct) {
+    long long rank = (long long)ceil(__dmul_rn(pct, (double)n));
+    if (rank < 1) rank = 1;
+    if (rank > n) rank = n;
+    return v[rank - 1];
+}
+
+__global__ void summary_kernel(const MetricParams* params, const ReplicaDesc* desc,
+                               const ReplicaOut* out, const int4* spec, const RecOut* rec,
+                               RowArrays rows, const long long* echo, DevSummary* sum,
+                               int n_rep) {
+    int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (r >= n_rep) return;
+    const MetricParams mp = params[r];
+    const ReplicaOut o = out[r];
+    const long long base = mp.req_base, n = mp.n;
+    DevSummary s;
+    s.ttft_mean = s.ttft_p50 = s.ttft_p90 = s.ttft_p95 = s.ttft_p99 = 0.0;
+    s.slo_rate = s.ttfat_attain = s.throughput = 0.0;
+    s.capacity = echo[r];
+    s.requests = n;
+    s.req_iters = o.req_iters;
+    s.answer_tokens = o.answer_tokens;
+    s.events = o.events;
+    s.plans = o.plans;
+    s.visits = o.visits;
+    s.health = o.health_checks;
+    s.slo_violations = 0;
+    s.status = o.status;
+    s.pad = 0;
+    if (o.status == 0 && n > 0) {
+        long long viol = 0, ok = 0, tokens = 0;
+        double first = rec[base].arrival, last = rec[base].completion;
+        for (long long k = lane; k < n; k += 32) {
+            long long g = base + k;
+            viol += rows.slo[g];
+            ok += rows.ttfat[g] <= mp.ttfat_target ? 1 : 0;
+            int4 sp = spec[g];
+            tokens += (long long)sp.y + sp.z;
+            double a = rec[g].arrival, c = rec[g].completion;
+            first = a < first ? a : first;
+            last = last < c ? c : last;
+        }
+        for (int off = 16; off; off >>= 1) {
+            viol += __shfl_xor_sync(FULLM, viol, off);
+            ok += __shfl_xor_sync(FULLM, ok, off);
+            tokens += __shfl_xor_sync(FULLM, tokens, off);
+            double f2 = __shfl_xor_sync(FULLM, first, off);
+            double l2 = __shfl_xor_sync(FULLM, last, off);
+            first = f2 < first ? f2 : first;
+            last = last < l2 ? l2 : last;
+        }
+        if (lane == 0) {
+            const double* srt = rows.ttft_sorted + base;
+            double acc = 0.0;  // sorted-order sequential sum (metrics.cpp:139-143)
+            for (long long k = 0; k < n; ++k) acc = __dadd_rn(acc, srt[k]);
+            double dn = (double)n;
+            s.ttft_mean = __ddiv_rn(acc, dn);
+            s.ttft_p50 = nearest_rank(srt, n, 0.50);
+            s.ttft_p90 = nearest_rank(srt, n, 0.90);
+            s.ttft_p95 = nearest_rank(srt, n, 0.95);
+            s.ttft_p99 = nearest_rank(srt, n, 0.99);
+            s.slo_rate = __ddiv_rn((double)viol, dn);
+            s.ttfat_attain = __ddiv_rn((double)ok, dn);
+            s.slo_violations = viol;
+            double span = __dsub_rn(last, first);
+            s.throughput = span <= 0.0 ? 0.0 : __ddiv_rn((double)tokens, span);
+        }
+    }
+    if (lane == 0) sum[r] = s;
+}
+
+int launch_capacity(ReplicaDesc* desc, const ReplicaOut* oracle_out, const int* map,
+                    const double* fraction, const long long* biggest, long long* echo,
+                    int count, void* stream) {
+    if (count <= 0) return 0;
+    capacity_kernel<<<(count + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+        desc, oracle_out, map, fraction, biggest, echo, count);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int launch_metrics(const Arena& a, const MetricParams* params, const long long* seg,
+                   const int* rid, long long total, int n_rep, RowArrays rows,
+                   DevSummary* out, const long long* echo_capacity, void* sort_tmp,
+                   size_t* sort_tmp_bytes, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (sort_tmp == nullptr) {  // size query
+        size_t bytes = 0;
+        cudaError_t e = cub::DeviceSegmentedSort::SortKeys(
+            nullptr, bytes, rows.ttft, rows.ttft_sorted, (int)(total > 0 ? total : 1), n_rep,
+            seg, seg + 1, st);
+        *sort_tmp_bytes = bytes;
+        return e == cudaSuccess ? 0 : 1;
+    }
+    if (total > 0) {
+        rows_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(
+            rid, params, a.spec, a.aoff, a.rec, a.dig, a.ndel, rows, total);
+        size_t bytes = *sort_tmp_bytes;
+        if (cub::DeviceSegmentedSort::SortKeys(sort_tmp, bytes, rows.ttft, rows.ttft_sorted,
+                                               (int)total, n_rep, seg, seg + 1,
+                                               st) != cudaSuccess)
+            return 2;
+    }
+    summary_kernel<<<(n_rep * 32 + 127) / 128, 128, 0, st>>>(params, a.desc, a.out, a.spec,
+                                                              a.rec, rows, echo_capacity, out,
+                                                              n_rep);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+}  // namespace pb

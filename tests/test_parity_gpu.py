@@ -1,0 +1,43 @@
+"""Parity of the CUDA engine against the REAL reference (golden sha256 of
+records, decision logs and report files produced by oracle/make_golden.py from
+/root/reference) on every case of tests/cases.py. Bit-exact: decisions
+(admit / evict / block / migrate / demote order) and every double of every
+RequestRecord must match."""
+import os
+
+import pytest
+
+import paper_2602_11530_b200 as pb
+from cases import CASES
+from harness import (build_trace, first_diff, golden, make_cfg, make_profile, oracle_run,
+                     sha_file)
+
+GOLD = golden()
+PARAMS = [c for c in CASES if c["name"] in GOLD and c["size"] != "large"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c", PARAMS, ids=[c["name"] for c in PARAMS])
+def test_records_and_decision_log_bit_exact(c, tmp_path):
+    g = GOLD[c["name"]]
+    t = build_trace(c["trace"])
+    rec, ev = str(tmp_path / "gpu.rec"), str(tmp_path / "gpu.ev")
+    pb.run_dump(t, make_profile(c), make_cfg(c), rec, ev)
+    got_r, got_e = sha_file(rec), sha_file(ev)
+    if got_r != g["records"] or got_e != g["events"]:
+        orec, oev = oracle_run(c, t, str(tmp_path))
+        msg = f"records {got_r} vs {g['records']}\nevents {got_e} vs {g['events']}\n"
+        msg += "records diff:\n" + first_diff(rec, orec) + "\nevents diff:\n" + first_diff(ev, oev)
+        pytest.fail(msg)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c", PARAMS, ids=[c["name"] for c in PARAMS])
+def test_report_files_byte_identical(c, tmp_path):
+    g = GOLD[c["name"]]
+    t = build_trace(c["trace"])
+    prefix = str(tmp_path / "rep")
+    pb.run(t, make_profile(c), make_cfg(c), prefix)
+    for ext, want in g["report"].items():
+        assert sha_file(f"{prefix}.{ext}") == want, ext
+    assert pb.derive_capacity(t, make_profile(c), make_cfg(c)) == g["capacity"]
