@@ -1,0 +1,400 @@
+"""bench.py — scheduled request-iterations/s of the B200 PASCAL scheduling loop.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload c2|c1|c5] [--replicas R]
+
+Workload (default c2 = BASELINE.json configs[1]): "4 instances, 2k requests,
+Pascal with phase-boundary migration under tight KV-cache budget" — the
+reference CLI chat preset (proj/tools/pascalsim_cli.cpp:44-47), 2,000 requests
+at lambda = 12 req/s, 4 instances, capacity_fraction 0.3, policy pascal, the
+default DS-R1-32B LatencyProfile. One step simulates R independent replicas of
+that configuration per GPU (trace seeds 1.., weak scaling), each run to
+completion exactly as engine::run does (oracle capacity pre-run + policy run +
+metrics); units = request-iterations, identical for every
+policy. Multi-GPU: one process per GPU, disjoint seed shards, and one NCCL
+all-gather of the per-replica summaries (TTFT percentiles, SLO counters) at the
+end of each step; timing is the max over ranks of the device step time.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/ref_dump = /root/reference/proj compiled unmodified; falls back to
+the oracle port) on the same workload with all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "scheduled request-iterations/sec (1/2/4/8 B200) + P99 TTFT/SLO match vs CPU ref"
+UNIT = "request-iterations/s"
+CHAT = ("uniform:64:512", "hist:256=0.35,512=0.30,768=0.20,1024=0.10,1536=0.04,2048=0.01",
+        "uniform:256:1024")
+ACC_CHAT = ("uniform:64:512", "hist:256=0.35,512=0.30,768=0.20,1024=0.10,1536=0.04,2048=0.01",
+            "uniform:1024:4096")
+ACC_HEAVY = ("uniform:64:512", "uniform:2048:4608", "uniform:128:512")
+
+WORKLOADS = {
+    # label: (description, default replicas per GPU)
+    "c2": ("C2: chat preset, 2000 req, lambda 12, 4 instances, capacity_fraction 0.3, pascal",
+           296),
+    "c1": ("C1: chat preset, 64 req, lambda 12, 1 instance, capacity_fraction 0.5, pascal", 4736),
+    "c5": ("C5 slice: acceptance mixed 256 req, 4 instances, cap 0.5, lambda 2^(k/3), "
+           "4 policies", 4736),
+}
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def replica_specs(workload, rank, per_gpu):
+    """(trace recipe, cfg fields, profile fields) for this rank's replicas."""
+    out = []
+    for k in range(per_gpu):
+        g = rank * per_gpu + k
+        if workload == "c2":
+            out.append(({"gen": [2000, 12.0, *CHAT, 1 + g, False]},
+                        dict(policy="pascal", instance_count=4, capacity_fraction=0.3), {}))
+        elif workload == "c1":
+            out.append(({"gen": [64, 12.0, *CHAT, 1 + g, False]},
+                        dict(policy="pascal", instance_count=1, capacity_fraction=0.5), {}))
+        else:
+            seed, rest = divmod(g, 64)
+            kk, pol = divmod(rest, 4)
+            rate = 2.0 ** (kk / 3.0)
+            recipe = {"mix": [{"gen": [256, rate, *ACC_CHAT, seed, False]},
+                              {"gen": [256, rate, *ACC_HEAVY, seed + 1, False]}, 0.25, seed + 2]}
+            cfg = [dict(policy="pascal"), dict(policy="pascal", no_migration=1),
+                   dict(policy="pascal", non_adaptive=1), dict(policy="fcfs")][pol]
+            cfg.update(instance_count=4, capacity_fraction=0.5)
+            out.append((recipe, cfg, {"decode_base": 0.0003, "decode_per_request": 0.001}))
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        if shutil.which("nvidia-smi"):
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        busy = [x for x in sm if x > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def algorithmic_bytes(s):
+    """B = 16 V + 32 T + 16 T_ans + 16 H + 40 E."""
+    return (16 * s.candidate_visits + 32 * s.request_iterations + 16 * s.answer_tokens +
+            16 * s.health_checks + 40 * s.events)
+
+
+def ncu_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    w = d.get(workload) or {}
+    return w.get("dram_bytes_per_launch")
+
+
+def find_cpu_ref():
+    ref = os.path.join(ROOT, "oracle", "_ref", "ref_dump")
+    if os.path.exists(ref):
+        return ref, "reference"
+    port = os.path.join(ROOT, "oracle", "_build", "oracle_dump")
+    if not os.path.exists(port):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "restatement"],
+                       check=True)
+    return port, "port"
+
+
+def cpu_time_replicas(specs, procs, tmp):
+    """Run the CPU reference on `specs` with `procs` parallel processes; returns
+    (wall seconds, request-iterations)."""
+    import paper_2602_11530_b200 as pb
+    from cases import cfg_text
+    from harness import build_trace
+
+    exe, _ = find_cpu_ref()
+    jobs = []
+    units = 0
+    for i, (recipe, cfg, prof) in enumerate(specs):
+        t = build_trace(recipe)
+        units += t.request_iterations()
+        hexp = os.path.join(tmp, f"r{i}.hex")
+        t.save_hex(hexp)
+        cfgp = os.path.join(tmp, f"r{i}.cfg")
+        with open(cfgp, "w") as f:
+            f.write(cfg_text({"cfg": cfg, "profile": prof}))
+        jobs.append([exe, "run", hexp, cfgp, os.path.join(tmp, f"r{i}.rec"), "-"])
+    t0 = time.perf_counter()
+    running = []
+    for j in jobs:
+        while len(running) >= procs:
+            running.pop(0).wait()
+        running.append(subprocess.Popen(j, stdout=subprocess.DEVNULL))
+    for p in running:
+        p.wait()
+    return time.perf_counter() - t0, units
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU scheduler on all host cores."""
+    cores = os.cpu_count() or 1
+    if rank != 0:
+        return
+    exe, kind = find_cpu_ref()
+    desc, _ = WORKLOADS[args.workload]
+    # bounded sample per step: one replica per host core (whole replicas, never truncated)
+    per_step = args.ref_replicas or cores
+    specs = replica_specs(args.workload, 0, per_step)
+    with tempfile.TemporaryDirectory() as tmp:
+        for _ in range(args.warmup):  # warm-up: a single small replica (page-in, caches)
+            cpu_time_replicas(replica_specs("c1", 0, 1), 1, tmp)
+        times, units = [], 0
+        for _ in range(args.steps):
+            dt, u = cpu_time_replicas(specs, cores, tmp)
+            times.append(dt)
+            units = u
+    tot = sum(times)
+    value = units * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator, seeds 1..)",
+        "config": {"workload": desc, "replicas_per_step": per_step,
+                   "timed": "engine::run incl. capacity pre-run, one process per replica"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(cores, per_step),
+                         "kind": kind, "sample": f"{per_step} whole {args.workload} replicas "
+                                                 f"per step, {cores} host cores"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--replicas", type=int, default=0, help="replicas per GPU per step")
+    ap.add_argument("--ref-replicas", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_11530_b200 as pb
+    from harness import build_trace
+
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    pb.set_device(local)
+    desc, default_r = WORKLOADS[args.workload]
+    per_gpu = args.replicas or default_r
+    specs = replica_specs(args.workload, rank, per_gpu)
+    traces = [build_trace(r) for r, _, _ in specs]
+    cfgs = [pb.run_config(**c) for _, c, _ in specs]
+    profs = [pb.Profile.default(**p) for _, _, p in specs]
+    units = sum(t.request_iterations() for t in traces)
+
+    # ---- device-resident batch: value (inputs already in HBM)
+    batch = pb.Batch(traces, profs, cfgs)
+    dev = torch.device("cuda", local)
+
+    def gather(summ):
+        """NCCL all-gather of per-replica summaries (TTFT P50/P99, SLO counts)."""
+        if world == 1:
+            return None
+        x = torch.tensor([[s.ttft_p50, s.ttft_p99, float(s.slo_violations), float(s.requests),
+                           float(s.status)] for s in summ], dtype=torch.float64, device=dev)
+        out = [torch.empty_like(x) for _ in range(world)]
+        dist.all_gather(out, x)
+        return torch.cat(out)
+
+    for _ in range(args.warmup):
+        batch.execute()
+        gather(batch.summaries())
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, engine_ms, launches = [], [], 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            batch.execute()
+            tm = pb.last_timing()
+            summ = batch.summaries()
+            gather(summ)
+            step_ms.append(tm.total_ms)
+            engine_ms.append(tm.engine_ms)
+            launches += tm.kernel_launches
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    bad = [s.status for s in summ if s.status != 0]
+    if bad:
+        raise SystemExit(f"replica failures: {bad[:5]}")
+    my_ms = sum(step_ms) / len(step_ms)
+    t = torch.tensor([my_ms, sum(engine_ms) / len(engine_ms)], dtype=torch.float64)
+    tot_units = units
+    if world > 1:
+        tt = t.to(dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = tt.cpu()
+        u = torch.tensor([units], dtype=torch.float64, device=dev)
+        dist.all_reduce(u)
+        tot_units = int(u.item())
+    ms_step, ms_engine = float(t[0]), float(t[1])
+    value = tot_units / (ms_step / 1000.0)
+    del batch
+
+    # ---- e2e through the public C-ABI call with host buffers (H2D + D2H inside)
+    e2e_times = []
+    for i in range(max(1, min(args.steps, 3))):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        summ2 = pb.run_batch(traces, profs, cfgs)
+        e2e_times.append(time.perf_counter() - t0)
+        tm2 = pb.last_timing()
+    e2e_s = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64)
+    if world > 1:
+        e2e_d = e2e_s.to(dev)
+        dist.all_reduce(e2e_d, op=dist.ReduceOp.MAX)
+        e2e_s = e2e_d.cpu()
+    e2e_value = tot_units / float(e2e_s[0])
+    assert [s.ttft_p99 for s in summ2] == [s.ttft_p99 for s in summ]
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline for the dominant kernel (policy-run sched_kernel launch)
+    peak, peak_src = load_peaks()
+    alg = sum(algorithmic_bytes(s) for s in summ)
+    achieved = alg / (ms_engine / 1000.0) / 1e9
+    traffic = ncu_traffic(args.workload)
+    p99 = sorted(s.ttft_p99 for s in summ)
+    slo = sum(s.slo_violations for s in summ) / max(1, sum(s.requests for s in summ))
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        exe, kind = find_cpu_ref()
+        with tempfile.TemporaryDirectory() as tmp:
+            dt, u = cpu_time_replicas(specs[:1], 1, tmp)
+        cpu = {"value": u / dt, "unit": UNIT, "cores": 1, "kind": kind,
+               "sample": f"1 whole {args.workload} replica (seed 1), engine::run incl. capacity "
+                         f"pre-run, single thread"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference trace generator, seeds 1..)",
+        "config": {"workload": desc, "replicas_per_gpu": per_gpu,
+                   "request_iterations_per_step": tot_units,
+                   "timed": "oracle capacity pre-run + policy run + metrics, all on device",
+                   "l2": "inputs larger than L2 (per-replica arenas > 126 MB total)",
+                   "parallelism": f"replica shards x{world}"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(tm2.h2d_bytes),
+                "d2h_bytes_per_step": int(tm2.d2h_bytes)},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "pb::sched_kernel (policy run)", "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg,
+                     "kernel_ms": ms_engine},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "results": {"ttft_p99_median_over_replicas": p99[len(p99) // 2],
+                    "slo_violation_rate": slo},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -49,7 +49,9 @@ struct DevBuf {
     }
 };
 
-constexpr int kWarpsPerBlock = 4;
+// Replicas per CTA: one warp each. Few replicas -> one warp per CTA so they
+// spread over all 148 SMs; many -> four per CTA (one per SM sub-partition).
+int warps_per_block(int reps, int sms) { return std::max(1, std::min(4, reps / std::max(1, sms))); }
 constexpr long long kMaxReq = (1ll << 26) - 1;  // heap id field
 constexpr int kMaxInst = 512;
 
@@ -369,9 +371,10 @@ void Batch::execute() {
     build();
     Timing& tm = g_timing;
     const int sms = sm_count();
-    auto blocks_for = [&](int reps) {
-        int want = (reps + kWarpsPerBlock - 1) / kWarpsPerBlock;
-        return std::max(1, std::min(want, sms * 8));
+    auto launch = [&](const pb::Arena& ar, int reps) {
+        const int wpb = warps_per_block(reps, sms);
+        const int blocks = std::max(1, std::min((reps + wpb - 1) / wpb, sms * 8));
+        return pb::launch_engine(ar, max_ni_, wpb, blocks, st_);
     };
     int launches = 0;
     ck(cudaEventRecord(ev_[0], st_), "event");
@@ -381,7 +384,7 @@ void Batch::execute() {
     ck(cudaMemsetAsync(d_work_.p, 0, 2 * sizeof(int), st_), "memset");
     if (!odesc_.empty()) {
         pb::Arena oa = arena(true);
-        if (pb::launch_engine(oa, max_ni_, kWarpsPerBlock, blocks_for((int)odesc_.size()), st_))
+        if (launch(oa, (int)odesc_.size()))
             throw std::logic_error("engine launch failed (oracle pre-run)");
         if (pb::launch_capacity(d_desc_.p, d_oout_.p, d_omap_.p, d_frac_.p, d_biggest_.p,
                                 d_echo_.p, (int)odesc_.size(), st_))
@@ -390,7 +393,7 @@ void Batch::execute() {
     }
     ck(cudaEventRecord(ev_[1], st_), "event");
     pb::Arena pa = arena(false);
-    if (pb::launch_engine(pa, max_ni_, kWarpsPerBlock, blocks_for(n_rep_), st_))
+    if (launch(pa, n_rep_))
         throw std::logic_error("engine launch failed");
     launches += 1;
     ck(cudaEventRecord(ev_[2], st_), "event");

@@ -41,3 +41,23 @@ def test_report_files_byte_identical(c, tmp_path):
     for ext, want in g["report"].items():
         assert sha_file(f"{prefix}.{ext}") == want, ext
     assert pb.derive_capacity(t, make_profile(c), make_cfg(c)) == g["capacity"]
+
+
+LARGE = [c for c in CASES if c["name"] in GOLD and c["size"] == "large"]
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("c", LARGE, ids=[c["name"] for c in LARGE])
+def test_large_bit_exact(c, tmp_path):
+    """C2 (BASELINE.json configs[1]) at full size: 18.5 M decision-log lines."""
+    g = GOLD[c["name"]]
+    t = build_trace(c["trace"])
+    rec, ev = str(tmp_path / "gpu.rec"), str(tmp_path / "gpu.ev")
+    pb.run_dump(t, make_profile(c), make_cfg(c), rec, ev)
+    assert sha_file(rec) == g["records"]
+    assert sha_file(ev) == g["events"]
+    prefix = str(tmp_path / "rep")
+    pb.run(t, make_profile(c), make_cfg(c), prefix)
+    for ext, want in g["report"].items():
+        assert sha_file(f"{prefix}.{ext}") == want, ext
