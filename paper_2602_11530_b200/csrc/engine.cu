@@ -709,6 +709,20 @@ DEVI void order_segment(const Rep& R, int s, int e, unsigned qmin, unsigned qmax
     __syncwarp();
 }
 
+// Highest candidate index j < b with a resident KV footprint (a potential
+// back-region victim), or -1.
+DEVI int find_rb(const Rep& R, int b) {
+    for (int hi = b; hi > 0; hi -= 32) {
+        int lo = max(0, hi - 32);
+        int j = lo + lane_id();
+        bool res = false;
+        if (j < hi) res = cand_rkv(R.cand[j]) > 0;
+        unsigned mk = __ballot_sync(FULL, res);
+        if (mk) return lo + 31 - __clz(mk);
+    }
+    return -1;
+}
+
 // maybe_start (engine.cpp:192-258) with plan_iteration (instance.cpp:103-282).
 DEVI void maybe_start(const Rep& R, Scal& S, int i) {
     if (R.s.busy[i]) return;
@@ -747,90 +761,130 @@ DEVI void maybe_start(const Rep& R, Scal& S, int i) {
     }
 
     // ---- admission / controlled preemption (instance.cpp:143-243)
+    // Warp-parallel greedy with an exact scalar slow path. Per chunk of 32
+    // candidates, everything up to the first "event" is decided at once:
+    //   * evicted earlier in the pass (index >= b, resident)      -> deny
+    //   * FCFS strict queue after a denial                        -> deny
+    //   * need <= free after the admitted prefix (prefix sum)      -> admit
+    //   * need > free at chunk state with no reachable victim,
+    //     not resident, not FCFS, something already admitted      -> deny
+    // The first candidate that may evict, deny a resident (stack push), set
+    // the FCFS block, or reach the deadlock breaker runs the reference logic
+    // one candidate at a time (walk_back / pop_stack). rb = highest resident
+    // index below b, so "a victim exists in [lo, b)" is rb >= lo.
     Adm A;
     A.free_ = R.cap - R.s.gpu[i];
     A.b = n;
     A.ns = 0;
     A.ne = 0;
+    int stack_top = -1;
+    int rb = find_rb(R, n);
     bool any_admitted = false, fcfs_blocked = false;
     const bool fcfs = R.policy == kFcfs, oracle = R.policy == kOracle;
+    // materialisation statistics, accumulated as candidates are decided
+    // (instance.cpp:245-267): first admitted waiting-prefill, batch size/KV,
+    // swap-ins, immediate swap-ins, denials
+    int pf = INT_MAX;
+    long long bcount = 0, bkv = 0;
+    int nsw = 0, nimm = 0, nden = 0;
+    const int ln = lane_id();
     for (int base = 0; base < n; base += 32) {
+        const int ci_l = base + ln;
+        const bool valid = ci_l < n;
         int4 my = make_int4(0, 0, 0, 0);
-        if (base + lane_id() < n) my = R.cand[base + lane_id()];
+        if (valid) my = R.cand[ci_l];
+        const long long my_need = my.y;
+        const int my_rkv = cand_rkv(my);
+        const int my_w = my.w;
+        const bool my_allow = !oracle && !(fcfs && (my_w & CF_WAIT));
+        const int my_s = classed ? ((my_w & CF_LOW) ? c1 : k0) : 0;
         unsigned char st = 0;
-        int cnt = min(32, n - base);
-        for (int k = 0; k < cnt; ++k) {
-            int ci = base + k;
-            int cx = __shfl_sync(FULL, my.x, k);
-            long long need = __shfl_sync(FULL, my.y, k);
-            int cz = __shfl_sync(FULL, my.z, k);
-            int cw = __shfl_sync(FULL, my.w, k);
-            int rkv = ((cw & CF_RES) && cz > 0) ? cz : 0;
-            unsigned char dec;
-            if ((ci >= A.b && rkv > 0) || (fcfs_blocked && rkv == 0)) {
-                dec = CS_DENY;  // evicted earlier in this pass, or FCFS strict queue
-            } else {
-                if (need > A.free_) {
-                    bool allow = !oracle && !(fcfs && (cw & CF_WAIT));
-                    if (allow) {
-                        int s = classed ? ((cw & CF_LOW) ? c1 : k0) : 0;
-                        walk_back(R, A, max(s, ci + 1), need);
-                        pop_stack(R, A, s, need);
-                        if (need > A.free_ && !any_admitted) {  // deadlock breaker :211-220
-                            walk_back(R, A, ci + 1, need);
-                            pop_stack(R, A, 0, need);
-                        }
+        const int cnt = min(32, n - base);
+        int k = 0;
+        while (k < cnt) {
+            const bool mine = valid && ln >= k;
+            const bool evd = mine && ci_l >= A.b && my_rkv > 0;
+            const bool bld = mine && !evd && fcfs_blocked && my_rkv == 0;
+            const bool act = mine && !evd && !bld;
+            const long long F = A.free_;
+            const bool sf = act && my_need > F;
+            const bool vict =
+                my_allow && (rb >= max(my_s, ci_l + 1) || (A.ns > 0 && stack_top >= my_s));
+            const bool simple_sf = sf && my_rkv == 0 && !fcfs && any_admitted && !vict;
+            const bool fc = act && !sf;
+            long long contrib = fc ? my_need : 0;
+            long long pin = contrib;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                long long y = __shfl_up_sync(FULL, pin, o);
+                if (ln >= o) pin += y;
+            }
+            const bool stop_here = (fc && pin > F) || (sf && !simple_sf);
+            const unsigned sm = __ballot_sync(FULL, stop_here);
+            const int stop = sm ? __ffs(sm) - 1 : cnt;
+            const bool fin = mine && ln < stop;
+            if (fin) st = fc ? CS_ADMIT : CS_DENY;
+            const long long taken = warp_sum_ll(fin ? contrib : 0);
+            A.free_ -= taken;
+            if (__ballot_sync(FULL, fin && fc)) any_admitted = true;
+            if (stop >= cnt) break;
+            // ---- exact reference step for candidate `stop`
+            const int ci = base + stop;
+            const long long need = __shfl_sync(FULL, my_need, stop);
+            const int cw = __shfl_sync(FULL, my_w, stop);
+            const int rkv = __shfl_sync(FULL, my_rkv, stop);
+            const int b0 = A.b;
+            if (need > A.free_) {
+                bool allow = !oracle && !(fcfs && (cw & CF_WAIT));
+                if (allow) {
+                    int s = classed ? ((cw & CF_LOW) ? c1 : k0) : 0;
+                    walk_back(R, A, max(s, ci + 1), need);
+                    pop_stack(R, A, s, need);
+                    if (need > A.free_ && !any_admitted) {  // deadlock breaker :211-220
+                        walk_back(R, A, ci + 1, need);
+                        pop_stack(R, A, 0, need);
                     }
-                }
-                if (need <= A.free_) {
-                    dec = CS_ADMIT;
-                    any_admitted = true;
-                    A.free_ -= need;
-                } else {
-                    dec = CS_DENY;
-                    if (rkv > 0) {
-                        if (lane_id() == 0) R.stack[A.ns] = (unsigned)ci;
-                        A.ns++;
-                    }
-                    if (fcfs) fcfs_blocked = true;
                 }
             }
-            (void)cx;
-            if (lane_id() == k) st = dec;
+            unsigned char dec;
+            if (need <= A.free_) {
+                dec = CS_ADMIT;
+                any_admitted = true;
+                A.free_ -= need;
+            } else {
+                dec = CS_DENY;
+                if (rkv > 0) {
+                    if (ln == 0) R.stack[A.ns] = (unsigned)ci;
+                    A.ns++;
+                }
+                if (fcfs) fcfs_blocked = true;
+            }
+            stack_top = A.ns > 0 ? (int)R.stack[A.ns - 1] : -1;
+            if (A.b != b0) rb = find_rb(R, A.b);
+            if (ln == stop) st = dec;
+            k = stop + 1;
         }
-        if (base + lane_id() < n) R.cstat[base + lane_id()] = st;
+        if (valid) R.cstat[ci_l] = st;
+        // statistics for this (now final) chunk
+        const bool adm = st == CS_ADMIT, den = st == CS_DENY;
+        bool wt = false, inb = false, sw = false, imm = false;
+        if (adm) {
+            if (my_w & CF_WAIT) wt = true;
+            else if (my_w & CF_RES) inb = true;
+            else if (swap_latency(R.prof, my.z) == 0.0) { imm = true; inb = true; }
+            else sw = true;
+        }
+        const unsigned wm = __ballot_sync(FULL, wt);
+        if (wm && pf == INT_MAX) pf = base + __ffs(wm) - 1;
+        bcount += __popc(__ballot_sync(FULL, inb));
+        bkv += warp_sum_ll(inb ? (long long)my.z : 0);
+        nsw += __popc(__ballot_sync(FULL, sw));
+        nimm += __popc(__ballot_sync(FULL, imm));
+        nden += __popc(__ballot_sync(FULL, den));
         __syncwarp();
     }
     if (A.free_ < 0) pop_stack(R, A, 0, 0);  // over-capacity repair :235-243
 
-    // ---- materialise (instance.cpp:245-281): pass A, statistics
-    int pf = INT_MAX;
-    long long bcount = 0, bkv = 0;
-    int nsw = 0, nimm = 0, nden = 0;
-    for (int base = 0; base < n; base += 32) {
-        int k = base + lane_id();
-        bool adm = false, den = false, wt = false, inb = false, sw = false, imm = false;
-        int4 c = make_int4(0, 0, 0, 0);
-        if (k < n) {
-            c = R.cand[k];
-            unsigned char st = R.cstat[k];
-            adm = st == CS_ADMIT;
-            den = st == CS_DENY;
-        }
-        if (adm) {
-            if (c.w & CF_WAIT) wt = true;
-            else if (c.w & CF_RES) inb = true;
-            else if (swap_latency(R.prof, c.z) == 0.0) { imm = true; inb = true; }
-            else sw = true;
-        }
-        unsigned wm = __ballot_sync(FULL, wt);
-        if (wm && pf == INT_MAX) pf = base + __ffs(wm) - 1;
-        bcount += __popc(__ballot_sync(FULL, inb));
-        bkv += warp_sum_ll(inb ? (long long)c.z : 0);
-        nsw += __popc(__ballot_sync(FULL, sw));
-        nimm += __popc(__ballot_sync(FULL, imm));
-        nden += __popc(__ballot_sync(FULL, den));
-    }
     int kind;  // 0 idle, 1 prefill, 2 decode
     double dur;
     int pf_idx = -1;
