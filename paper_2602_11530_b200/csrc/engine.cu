@@ -163,16 +163,17 @@ struct Rep {
     long long logcap;
     // request arrays (offset to this replica)
     const double* arrival;
-    const int4* spec;
-    const long long* aoff;
+    int4* spec;
+    int* aoff;  // answer-slot offset relative to dig / del
     int4* hot;
     unsigned* meta;
     int* qused;
     int* ndel;
     int* cursor;
+    double* blocked;
     RecOut* rec;
-    double* dig;
-    double* del;
+    double* dig;  // this replica's digest arena
+    double* del;  // this replica's delivery arena
     uint2* qent;
     long long qcap;
     unsigned* batch;
@@ -181,6 +182,16 @@ struct Rep {
     int4* tmp;
     unsigned* tmpq;
     unsigned char* cstat;
+    // candidate scratch: shared memory (capacity c_smem) and HBM (capacity n)
+    int4* s_cand;
+    int4* s_tmp;
+    unsigned* s_tmpq;
+    unsigned char* s_cstat;
+    int4* g_cand;
+    int4* g_tmp;
+    unsigned* g_tmpq;
+    unsigned char* g_cstat;
+    int c_smem;
     unsigned* elist;
     unsigned* stack;
     LogEnt* log;
@@ -519,10 +530,11 @@ DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
 // (PacerState::on_delivery, instance.cpp:10-20 + engine.cpp:148-156).
 DEVI void deliver_lane(const Rep& R, double now, int idx, double iter_start) {
     int nd = R.ndel[idx];
-    double* d = R.dig + R.aoff[idx];
+    const int off = R.aoff[idx];
+    double* d = R.dig + off;
     double v = nd == 0 ? now : dmax(now, __dadd_rn(d[nd - 1], R.tpot));
     d[nd] = v;
-    if (R.flags & kRecordDeliv) R.del[R.aoff[idx] + nd] = now;
+    if (R.flags & kRecordDeliv) R.del[off + nd] = now;
     R.ndel[idx] = nd + 1;
     if (nd == 0) {
         R.rec[idx].first_answer_delivery = now;
@@ -724,9 +736,22 @@ DEVI int find_rb(const Rep& R, int b) {
 }
 
 // maybe_start (engine.cpp:192-258) with plan_iteration (instance.cpp:103-282).
-DEVI void maybe_start(const Rep& R, Scal& S, int i) {
+DEVI void maybe_start(Rep& R, Scal& S, int i) {
     if (R.s.busy[i]) return;
     S.plans++;
+    // candidates never exceed the queued entries: use the shared-memory
+    // scratch when they fit
+    if (R.s.hi_len[i] + R.s.lo_len[i] <= R.c_smem) {
+        R.cand = R.s_cand;
+        R.tmp = R.s_tmp;
+        R.tmpq = R.s_tmpq;
+        R.cstat = R.s_cstat;
+    } else {
+        R.cand = R.g_cand;
+        R.tmp = R.g_tmp;
+        R.tmpq = R.g_tmpq;
+        R.cstat = R.g_cstat;
+    }
     const bool pascal = R.policy == kPascal;
     const bool classed = pascal;
 
@@ -968,8 +993,7 @@ DEVI void maybe_start(const Rep& R, Scal& S, int i) {
             log_put(R, limm + __popc(imm_m & lt), S.now, kLSwapIn, i, c.x, 0);
         }
         if (den) {
-            RecOut* rc = &R.rec[c.x];
-            rc->blocked = __dadd_rn(rc->blocked, dur);
+            R.blocked[c.x] = __dadd_rn(R.blocked[c.x], dur);
             log_put(R, lden + __popc(dnm & lt), S.now, kLBlock, i, c.x, 0);
         }
         if (inb && kind == 2) bout[bpos + __popc(bm & lt)] = (unsigned)c.x;
@@ -1020,7 +1044,7 @@ DEVI void maybe_start(const Rep& R, Scal& S, int i) {
 
 // --------------------------------------------------------------- events
 // engine.cpp:260-283
-DEVI void on_arrival(const Rep& R, Scal& S, int idx) {
+DEVI void on_arrival(Rep& R, Scal& S, int idx) {
     if (lane_id() == 0) R.rec[idx].arrival = S.now;
     const bool pascal = R.policy == kPascal;
     if (pascal) compute_health(R, S);
@@ -1052,7 +1076,7 @@ DEVI void on_arrival(const Rep& R, Scal& S, int idx) {
 }
 
 // engine.cpp:285-308
-DEVI void on_prefill_complete(const Rep& R, Scal& S, int idx) {
+DEVI void on_prefill_complete(Rep& R, Scal& S, int idx) {
     unsigned m = R.meta[idx];
     int i = m_owner(m);
     int4 sp = R.spec[idx];
@@ -1104,7 +1128,7 @@ DEVI void on_prefill_complete(const Rep& R, Scal& S, int idx) {
 }
 
 // engine.cpp:310-337: retire one decode iteration, batch members in plan order.
-DEVI void on_iteration_complete(const Rep& R, Scal& S, int i) {
+DEVI void on_iteration_complete(Rep& R, Scal& S, int i) {
     if (lane_id() == 0) R.s.busy[i] = 0;
     int nb = R.s.blen[i];
     double iter_start = R.s.iter_start[i];
@@ -1212,7 +1236,7 @@ DEVI void on_iteration_complete(const Rep& R, Scal& S, int i) {
 }
 
 // engine.cpp:339-349
-DEVI void on_swap_complete(const Rep& R, Scal& S, int idx) {
+DEVI void on_swap_complete(Rep& R, Scal& S, int idx) {
     unsigned m = R.meta[idx];
     int i = m_owner(m);
     if (lane_id() == 0) {
@@ -1227,7 +1251,7 @@ DEVI void on_swap_complete(const Rep& R, Scal& S, int idx) {
 }
 
 // engine.cpp:351-367
-DEVI void on_transfer_complete(const Rep& R, Scal& S, int idx) {
+DEVI void on_transfer_complete(Rep& R, Scal& S, int idx) {
     unsigned m = R.meta[idx];
     int dst = m_owner(m);
     long long kv = R.hot[idx].x;
@@ -1249,7 +1273,7 @@ DEVI void on_transfer_complete(const Rep& R, Scal& S, int idx) {
 }
 
 // ------------------------------------------------------------ the replica
-DEVI void run_replica(const Arena& a, int r, char* smem) {
+DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem, int c_smem) {
     const ReplicaDesc d = a.desc[r];
     Rep R;
     R.n = d.n;
@@ -1264,30 +1288,26 @@ DEVI void run_replica(const Arena& a, int r, char* smem) {
     R.prof = d.prof;
     R.logcap = d.log_cap;
     const long long g = d.req_base;
+    const long long abase = R.n > 0 ? a.aoff[g] : 0;
     R.arrival = a.arrival + g;
-    R.spec = a.spec + g;
-    R.aoff = a.aoff + g;
-    R.hot = a.hot + g;
-    R.meta = a.meta + g;
-    R.qused = a.qused + g;
-    R.ndel = a.ndel + g;
-    R.cursor = a.cursor + g;
     R.rec = a.rec + g;
-    R.dig = a.dig;
-    R.del = a.del;
+    R.dig = a.dig + abase;
+    R.del = a.del + abase;
     R.qent = a.qent + d.queue_base;
     R.qcap = d.qcap;
     R.batch = a.batch + d.batch_base;
     R.heap = a.heap + d.heap_base;
-    R.cand = a.cand + g;
-    R.tmp = a.tmp + g;
-    R.tmpq = a.tmpq + g;
-    R.cstat = a.cstat + g;
+    R.g_cand = a.cand + g;
+    R.g_tmp = a.tmp + g;
+    R.g_tmpq = a.tmpq + g;
+    R.g_cstat = a.cstat + g;
     R.elist = a.elist + g;
     R.stack = a.stack + g;
     R.log = a.log + d.log_base;
     const int ni = d.ni;
-    R.s.gpu = reinterpret_cast<long long*>(smem);
+    // ---- shared-memory carve-up (engine.h smem_per_warp)
+    char* sp = smem;
+    R.s.gpu = reinterpret_cast<long long*>(sp);
     R.s.cpu = R.s.gpu + ni;
     R.s.iter_start = reinterpret_cast<double*>(R.s.cpu + ni);
     R.s.link = R.s.iter_start + ni;
@@ -1299,6 +1319,35 @@ DEVI void run_replica(const Arena& a, int r, char* smem) {
     R.s.blen = R.s.afresh + ni;
     R.s.busy = R.s.blen + ni;
     R.s.healthy = R.s.busy + ni;
+    sp += smem_inst_bytes(max_ni);
+    const bool resident = R.n <= n_smem;  // request state in shared memory
+    if (resident) {
+        R.hot = reinterpret_cast<int4*>(sp);
+        R.spec = R.hot + n_smem;
+        R.blocked = reinterpret_cast<double*>(R.spec + n_smem);
+        R.meta = reinterpret_cast<unsigned*>(R.blocked + n_smem);
+        R.qused = reinterpret_cast<int*>(R.meta + n_smem);
+        R.ndel = R.qused + n_smem;
+        R.cursor = R.ndel + n_smem;
+        R.aoff = R.cursor + n_smem;
+    } else {
+        R.hot = a.hot + g;
+        R.spec = const_cast<int4*>(a.spec) + g;
+        R.blocked = a.blocked + g;
+        R.meta = a.meta + g;
+        R.qused = a.qused + g;
+        R.ndel = a.ndel + g;
+        R.cursor = a.cursor + g;
+        R.aoff = const_cast<int*>(a.aoff32) + g;
+    }
+    sp += smem_req_bytes(n_smem);
+    if (resident) R.heap = reinterpret_cast<HeapEnt*>(sp);
+    sp += smem_heap_bytes(n_smem, max_ni);
+    R.c_smem = c_smem;
+    R.s_cand = reinterpret_cast<int4*>(sp);
+    R.s_tmp = R.s_cand + c_smem;
+    R.s_tmpq = reinterpret_cast<unsigned*>(R.s_tmp + c_smem);
+    R.s_cstat = reinterpret_cast<unsigned char*>(R.s_tmpq + c_smem);
     for (int i = lane_id(); i < ni; i += 32) {
         R.s.gpu[i] = 0;
         R.s.cpu[i] = 0;
@@ -1315,6 +1364,11 @@ DEVI void run_replica(const Arena& a, int r, char* smem) {
         R.qused[k] = 0;
         R.ndel[k] = 0;
         R.cursor[k] = 0;
+        R.blocked[k] = 0.0;
+        if (resident) {
+            R.spec[k] = a.spec[g + k];
+            R.aoff[k] = a.aoff32[g + k];
+        }
         RecOut z;
         z.arrival = z.prefill_complete = z.reasoning_end = z.first_answer_delivery = 0.0;
         z.first_answer_iter_start = z.blocked = z.completion = z.mig_start = z.mig_end = 0.0;
@@ -1377,6 +1431,11 @@ DEVI void run_replica(const Arena& a, int r, char* smem) {
         if (S.hn + 1 > heap_cap && S.status == 0) S.status = kErrHeap;
     }
     if (S.status == 0 && S.done != R.n) S.status = kErrStall;
+    // outputs the metric kernels read: delivered counts and blocked totals
+    for (int k = lane_id(); k < R.n; k += 32) {
+        R.rec[k].blocked = R.blocked[k];
+        if (resident) a.ndel[g + k] = R.ndel[k];
+    }
     if (lane_id() == 0) {
         ReplicaOut o;
         o.status = S.status;
@@ -1395,28 +1454,30 @@ DEVI void run_replica(const Arena& a, int r, char* smem) {
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(128) sched_kernel(Arena a, int max_ni) {
+__global__ void __launch_bounds__(128) sched_kernel(Arena a, int max_ni, int n_smem, int c_smem) {
     extern __shared__ __align__(16) char smem_raw[];
     const int warp = threadIdx.x >> 5;
-    char* smem = smem_raw + warp * smem_per_warp(max_ni);
+    char* smem = smem_raw + (size_t)warp * smem_per_warp(max_ni, n_smem, c_smem);
     while (true) {
         int r = 0;
         if (lane_id() == 0) r = atomicAdd(a.work, 1);
         r = __shfl_sync(FULL, r, 0);
         if (r >= a.n_rep) break;
-        run_replica(a, r, smem);
+        run_replica(a, r, smem, max_ni, n_smem, c_smem);
     }
 }
 
-int launch_engine(const Arena& a, int max_ni, int warps_per_block, int blocks, void* stream) {
+int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int warps_per_block,
+                  int blocks, void* stream) {
     if (warps_per_block < 1 || warps_per_block > 4) return 1;
-    size_t smem = (size_t)warps_per_block * smem_per_warp(max_ni);
+    size_t smem = (size_t)warps_per_block * smem_per_warp(max_ni, n_smem, c_smem);
     if (smem > 48 * 1024) {
         if (cudaFuncSetAttribute(sched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) != cudaSuccess)
             return 2;
     }
-    sched_kernel<<<blocks, warps_per_block * 32, smem, (cudaStream_t)stream>>>(a, max_ni);
+    sched_kernel<<<blocks, warps_per_block * 32, smem, (cudaStream_t)stream>>>(a, max_ni, n_smem,
+                                                                               c_smem);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

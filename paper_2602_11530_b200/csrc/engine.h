@@ -110,12 +110,14 @@ struct Arena {
     const double* arrival;
     const int4* spec;       // {prompt, reasoning, answering, kv_preloaded}
     const long long* aoff;  // absolute offset of the request's answer slots
+    const int* aoff32;      // same, relative to the replica's first request
     // mutable request state
     int4* hot;        // {kv, tokens, enqueue_seq (0 = not queued), quanta_exhausted}
     unsigned* meta;   // phase:2 | loc:2 | swin:1 | swout:1 | qlow:1 | owner:16 (<<8)
     int* qused;       // quantum_used_in_round
     int* ndel;        // delivered answer tokens
     int* cursor;      // digests known <= a past `now` (pacer health cursor)
+    double* blocked;  // blocked_interval_total accumulator (global-resident replicas)
     RecOut* rec;
     double* dig;      // digest times (always)
     double* del;      // delivery times (kRecordDeliv)
@@ -167,12 +169,24 @@ struct RowArrays {
 #define PB_HD
 #endif
 
-// Dynamic shared memory per warp for ni instances.
-PB_HD inline int smem_per_warp(int ni) { return ni * 64 + 16; }
+// Dynamic shared memory per warp: instance state for ni instances; for
+// replicas with n <= n_smem also the hot per-request state (60 B each: hot,
+// spec, blocked, meta, quantum_used, delivered, cursor, answer offset) and
+// the event heap (n + ni + 2 entries of 16 B); and a candidate scratch of
+// c_smem entries (37 B each). Larger replicas keep request state and heap in
+// HBM; plans with more queued requests than c_smem use the HBM scratch.
+PB_HD inline int smem_inst_bytes(int ni) { return ((ni * 64 + 16) + 15) / 16 * 16; }
+PB_HD inline int smem_req_bytes(int n_smem) { return (n_smem * 60 + 15) / 16 * 16; }
+PB_HD inline int smem_heap_bytes(int n_smem, int ni) { return n_smem ? (n_smem + ni + 2) * 16 : 0; }
+PB_HD inline int smem_cand_bytes(int c_smem) { return (c_smem * 37 + 15) / 16 * 16; }
+PB_HD inline int smem_per_warp(int ni, int n_smem, int c_smem) {
+    return smem_inst_bytes(ni) + smem_req_bytes(n_smem) + smem_heap_bytes(n_smem, ni) +
+           smem_cand_bytes(c_smem);
+}
 
 // Host entries (engine.cu / metrics.cu). All enqueue on `stream`.
-int launch_engine(const Arena& a, int max_ni, int warps_per_block, int blocks,
-                  void* stream);
+int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int warps_per_block,
+                  int blocks, void* stream);
 // capacity = max(ceil(fraction * peak / ni), biggest) for the replicas listed
 // in `map` (derive_capacity, proj/src/engine.cpp:466-470); writes echo[r] and,
 // unless the replica runs the oracle policy, desc[r].capacity.

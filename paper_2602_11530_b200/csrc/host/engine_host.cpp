@@ -9,6 +9,8 @@
 // with PASCAL_ERR_INTERNAL.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <climits>
 #include <cstring>
@@ -49,18 +51,41 @@ struct DevBuf {
     }
 };
 
-// Replicas per CTA: one warp each. Few replicas -> one warp per CTA so they
-// spread over all 148 SMs; many -> four per CTA (one per SM sub-partition).
-int warps_per_block(int reps, int sms) { return std::max(1, std::min(4, reps / std::max(1, sms))); }
+// Launch shape. One warp per replica. The replica's hot request state and
+// the planner's candidate scratch go to shared memory when they fit (60 B per
+// request + 37 B per candidate slot); otherwise they stay in HBM. Few
+// replicas -> one warp per CTA so they spread over all SMs; many -> up to four
+// per CTA, as many as the shared-memory budget allows.
+struct Shape {
+    int n_smem, c_smem, wpb, blocks;
+};
+
+Shape pick_shape(int reps, int max_ni, int max_n) {
+    int dev = 0, sms = 148, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int budget = std::max(48 * 1024, optin) - 1024;
+    const char* env = std::getenv("PB_SMEM");
+    const bool allow_smem = !(env && env[0] == '0');
+    Shape sh{};
+    sh.c_smem = std::min(max_n, 1024);
+    sh.n_smem = allow_smem ? max_n : 0;
+    while (sh.n_smem > 0 && pb::smem_per_warp(max_ni, sh.n_smem, sh.c_smem) > budget)
+        sh.n_smem = 0;  // request state does not fit: HBM-resident replicas
+    while (pb::smem_per_warp(max_ni, sh.n_smem, sh.c_smem) > budget && sh.c_smem > 0)
+        sh.c_smem /= 2;
+    if (!allow_smem) sh.c_smem = 0;
+    const int per_warp = pb::smem_per_warp(max_ni, sh.n_smem, sh.c_smem);
+    const int fit = std::max(1, std::min(4, budget / per_warp));
+    sh.wpb = std::max(1, std::min(fit, reps / std::max(1, sms)));
+    const int per_sm = std::max(1, std::min(32 / sh.wpb, (228 * 1024) / (per_warp * sh.wpb)));
+    sh.blocks = std::max(1, std::min((reps + sh.wpb - 1) / sh.wpb, sms * per_sm));
+    return sh;
+}
 constexpr long long kMaxReq = (1ll << 26) - 1;  // heap id field
 constexpr int kMaxInst = 512;
 
-int sm_count() {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return sms;
-}
 
 void check_limits(const Job& j) {
     const RunCfg& c = j.cfg;
@@ -114,7 +139,7 @@ public:
     long long log_cap_ = 0;
     bool built_ = false;
 
-    int n_rep_ = 0, max_ni_ = 1;
+    int n_rep_ = 0, max_ni_ = 1, max_n_ = 0, max_on_ = 0;
     long long total_req_ = 0, total_ans_ = 0, total_q_ = 0, total_batch_ = 0, total_heap_ = 0,
               total_log_ = 0;
     std::vector<pb::ReplicaDesc> desc_;
@@ -131,7 +156,8 @@ public:
     DevBuf<int4> d_spec_, d_hot_, d_cand_, d_tmp_;
     DevBuf<long long> d_aoff_, d_biggest_, d_echo_, d_seg_;
     DevBuf<unsigned> d_meta_, d_batch_, d_tmpq_, d_elist_, d_stack_;
-    DevBuf<int> d_qused_, d_ndel_, d_cursor_;
+    DevBuf<int> d_qused_, d_ndel_, d_cursor_, d_aoff32_;
+    DevBuf<double> d_blocked_;
     DevBuf<pb::RecOut> d_rec_;
     DevBuf<double> d_dig_, d_del_;
     DevBuf<uint2> d_qent_;
@@ -226,6 +252,8 @@ void Batch::build() {
                                      (int)n, 0};
         seg[r] = rq;
         max_ni_ = std::max(max_ni_, ni);
+        max_n_ = std::max<int>(max_n_, (int)n);
+        if (j.cfg.gpu_capacity <= 0) max_on_ = std::max<int>(max_on_, (int)n);
         rq += n;
         for (const Spec& s : *j.trace) ans += s.answering;
         q += 2ll * ni * (n + 1);
@@ -245,17 +273,22 @@ void Batch::build() {
     std::vector<double> arrival(rq);
     std::vector<int4> spec(rq);
     std::vector<long long> aoff(rq);
+    std::vector<int> aoff32(rq);
     std::vector<int> rid(rq);
     long long g = 0, a = 0;
-    for (int r = 0; r < n_rep_; ++r)
+    for (int r = 0; r < n_rep_; ++r) {
+        const long long a0 = a;
         for (const Spec& s : *jobs_[r].trace) {
             arrival[g] = s.arrival;
             spec[g] = make_int4((int)s.prompt, (int)s.reasoning, (int)s.answering, s.preloaded ? 1 : 0);
             aoff[g] = a;
+            if (a - a0 > INT_MAX) throw std::invalid_argument("replica answer tokens exceed 2^31");
+            aoff32[g] = (int)(a - a0);
             rid[g] = r;
             a += s.answering;
             ++g;
         }
+    }
 
     // ---- device arenas
     d_desc_.ensure(n_rep_);
@@ -274,6 +307,8 @@ void Batch::build() {
     d_qused_.ensure(rq);
     d_ndel_.ensure(rq);
     d_cursor_.ensure(rq);
+    d_aoff32_.ensure(rq);
+    d_blocked_.ensure(rq);
     d_rec_.ensure(rq);
     d_cand_.ensure(rq);
     d_tmp_.ensure(rq);
@@ -323,6 +358,7 @@ void Batch::build() {
     up(d_arrival_.p, arrival.data(), arrival.size() * sizeof(double));
     up(d_spec_.p, spec.data(), spec.size() * sizeof(int4));
     up(d_aoff_.p, aoff.data(), aoff.size() * sizeof(long long));
+    up(d_aoff32_.p, aoff32.data(), aoff32.size() * sizeof(int));
     up(d_rid_.p, rid.data(), rid.size() * sizeof(int));
     up(d_params_.p, params.data(), params.size() * sizeof(pb::MetricParams));
     up(d_frac_.p, frac.data(), frac.size() * sizeof(double));
@@ -346,6 +382,8 @@ pb::Arena Batch::arena(bool oracle) const {
     a.arrival = d_arrival_.p;
     a.spec = d_spec_.p;
     a.aoff = d_aoff_.p;
+    a.aoff32 = d_aoff32_.p;
+    a.blocked = d_blocked_.p;
     a.hot = d_hot_.p;
     a.meta = d_meta_.p;
     a.qused = d_qused_.p;
@@ -370,11 +408,9 @@ pb::Arena Batch::arena(bool oracle) const {
 void Batch::execute() {
     build();
     Timing& tm = g_timing;
-    const int sms = sm_count();
-    auto launch = [&](const pb::Arena& ar, int reps) {
-        const int wpb = warps_per_block(reps, sms);
-        const int blocks = std::max(1, std::min((reps + wpb - 1) / wpb, sms * 8));
-        return pb::launch_engine(ar, max_ni_, wpb, blocks, st_);
+    auto launch = [&](const pb::Arena& ar, int reps, int max_n) {
+        const Shape sh = pick_shape(reps, max_ni_, max_n);
+        return pb::launch_engine(ar, max_ni_, sh.n_smem, sh.c_smem, sh.wpb, sh.blocks, st_);
     };
     int launches = 0;
     ck(cudaEventRecord(ev_[0], st_), "event");
@@ -384,7 +420,7 @@ void Batch::execute() {
     ck(cudaMemsetAsync(d_work_.p, 0, 2 * sizeof(int), st_), "memset");
     if (!odesc_.empty()) {
         pb::Arena oa = arena(true);
-        if (launch(oa, (int)odesc_.size()))
+        if (launch(oa, (int)odesc_.size(), max_on_))
             throw std::logic_error("engine launch failed (oracle pre-run)");
         if (pb::launch_capacity(d_desc_.p, d_oout_.p, d_omap_.p, d_frac_.p, d_biggest_.p,
                                 d_echo_.p, (int)odesc_.size(), st_))
@@ -393,7 +429,7 @@ void Batch::execute() {
     }
     ck(cudaEventRecord(ev_[1], st_), "event");
     pb::Arena pa = arena(false);
-    if (launch(pa, n_rep_))
+    if (launch(pa, n_rep_, max_n_))
         throw std::logic_error("engine launch failed");
     launches += 1;
     ck(cudaEventRecord(ev_[2], st_), "event");
