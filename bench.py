@@ -36,6 +36,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
+from paper_2602_11530_b200 import sweep  # noqa: E402
+
 METRIC = "scheduled request-iterations/sec (1/2/4/8 B200) + P99 TTFT/SLO match vs CPU ref"
 UNIT = "request-iterations/s"
 CHAT = ("uniform:64:512", "hist:256=0.35,512=0.30,768=0.20,1024=0.10,1536=0.04,2048=0.01",
@@ -73,15 +75,7 @@ def replica_specs(workload, rank, per_gpu):
             out.append(({"gen": [64, 12.0, *CHAT, 1 + g, False]},
                         dict(policy="pascal", instance_count=1, capacity_fraction=0.5), {}))
         else:
-            seed, rest = divmod(g, 64)
-            kk, pol = divmod(rest, 4)
-            rate = 2.0 ** (kk / 3.0)
-            recipe = {"mix": [{"gen": [256, rate, *ACC_CHAT, seed, False]},
-                              {"gen": [256, rate, *ACC_HEAVY, seed + 1, False]}, 0.25, seed + 2]}
-            cfg = [dict(policy="pascal"), dict(policy="pascal", no_migration=1),
-                   dict(policy="pascal", non_adaptive=1), dict(policy="fcfs")][pol]
-            cfg.update(instance_count=4, capacity_fraction=0.5)
-            out.append((recipe, cfg, {"decode_base": 0.0003, "decode_per_request": 0.001}))
+            out.append(sweep.replica_recipe(g))
     return out
 
 
@@ -191,7 +185,7 @@ def cpu_time_replicas(specs, procs, tmp):
         cfgp = os.path.join(tmp, f"r{i}.cfg")
         with open(cfgp, "w") as f:
             f.write(cfg_text({"cfg": cfg, "profile": prof}))
-        jobs.append([exe, "run", hexp, cfgp, os.path.join(tmp, f"r{i}.rec"), "-"])
+        jobs.append([exe, "sim", hexp, cfgp])
     t0 = time.perf_counter()
     running = []
     for j in jobs:
@@ -282,15 +276,25 @@ def main():
     batch = pb.Batch(traces, profs, cfgs)
     dev = torch.device("cuda", local)
 
+    base_id = rank * per_gpu
+    groups = [sweep.group_of(base_id + k) if args.workload == "c5" else 0
+              for k in range(per_gpu)]
+    ngroups = sweep.n_groups() if args.workload == "c5" else 1
+    batch.set_groups(groups, ngroups)
+
     def gather(summ):
-        """NCCL all-gather of per-replica summaries (TTFT P50/P99, SLO counts)."""
-        if world == 1:
-            return None
-        x = torch.tensor([[s.ttft_p50, s.ttft_p99, float(s.slo_violations), float(s.requests),
-                           float(s.status)] for s in summ], dtype=torch.float64, device=dev)
-        out = [torch.empty_like(x) for _ in range(world)]
-        dist.all_gather(out, x)
-        return torch.cat(out)
+        """End-of-step exchange: NCCL all-gather of per-replica summaries and
+        all-reduce of the device TTFT histograms / SLO counters."""
+        rows = torch.tensor([[float(base_id + k), s.ttft_mean, s.ttft_p50, s.ttft_p99,
+                              s.slo_violation_rate, s.throughput, float(s.requests),
+                              float(s.request_iterations), float(s.status)]
+                             for k, s in enumerate(summ)], dtype=torch.float64)
+        h, sl = batch.histograms()
+        h = torch.tensor(h, dtype=torch.int64)
+        sl = torch.tensor(sl, dtype=torch.int64)
+        if world > 1:
+            rows, h, sl = rows.to(dev), h.to(dev), sl.to(dev)
+        return sweep.reduce_results(rows, h, sl)
 
     for _ in range(args.warmup):
         batch.execute()
@@ -304,7 +308,7 @@ def main():
             batch.execute()
             tm = pb.last_timing()
             summ = batch.summaries()
-            gather(summ)
+            grows, ghist, gslo = gather(summ)
             step_ms.append(tm.total_ms)
             engine_ms.append(tm.engine_ms)
             launches += tm.kernel_launches
@@ -356,8 +360,10 @@ def main():
     alg = sum(algorithmic_bytes(s) for s in summ)
     achieved = alg / (ms_engine / 1000.0) / 1e9
     traffic = ncu_traffic(args.workload)
-    p99 = sorted(s.ttft_p99 for s in summ)
-    slo = sum(s.slo_violations for s in summ) / max(1, sum(s.requests for s in summ))
+    p99 = sorted(grows[:, 3].tolist())
+    tot_slo = gslo.sum(0).tolist()
+    slo = tot_slo[0] / max(1, tot_slo[1])
+    hist_all = ghist.sum(0).tolist()
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -387,7 +393,9 @@ def main():
                      "kernel_ms": ms_engine},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
-        "results": {"ttft_p99_median_over_replicas": p99[len(p99) // 2],
+        "results": {"replicas_all_ranks": len(p99),
+                    "ttft_p99_median_over_replicas": p99[len(p99) // 2],
+                    "ttft_p99_from_device_histogram": sweep.percentile_from_hist(hist_all, 0.99),
                     "slo_violation_rate": slo},
     }
     print(json.dumps(line), flush=True)

@@ -59,6 +59,17 @@ pascal_status pascal_batch_execute(pascal_batch* b);
 pascal_status pascal_batch_summaries(pascal_batch* b, pascal_summary* out);
 void pascal_batch_free(pascal_batch* b);
 
+/* Sweep reduction on the device: per-group TTFT histograms over every request
+ * of the group's replicas (PASCAL_HIST_BINS log-spaced bins over
+ * [1e-4, 1e5) s plus an underflow and an overflow bin) and SLO counters
+ * {violations, requests}. Groups are assigned once; the histograms are
+ * rebuilt by every pascal_batch_execute. */
+#define PASCAL_HIST_BINS 128
+pascal_status pascal_batch_set_groups(pascal_batch* b, const int* group_of_replica,
+                                      int n_groups);
+pascal_status pascal_batch_histograms(pascal_batch* b, unsigned long long* hist,
+                                      unsigned long long* slo);
+
 /* create + execute + summaries + free: the end-to-end replica-sweep call
  * with host buffers. */
 pascal_status pascal_run_batch(const pascal_trace* const* traces,

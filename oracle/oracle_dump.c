@@ -120,6 +120,17 @@ int main(int argc, char** argv) {
         po_dump_records(recs, n, f);
         fclose(f);
         po_records_free(recs, n);
+    } else if (!strcmp(argv[1], "sim")) {
+        po_record* recs = NULL;
+        if (po_run(t, n, &c, &p, NULL, &recs, err, sizeof err)) {
+            fprintf(stderr, "oracle_dump: %s\n", err);
+            return 1;
+        }
+        double last = 0.0;
+        for (long k = 0; k < n; ++k)
+            if (recs[k].completion > last) last = recs[k].completion;
+        printf("%ld %a\n", n, last);
+        po_records_free(recs, n);
     } else if (!strcmp(argv[1], "capacity")) {
         long cap = 0;
         if (po_derive_capacity(t, n, &c, &p, &cap, err, sizeof err)) {

@@ -8,6 +8,8 @@
 //   ref_dump capacity TRACE.hex CFG
 //   ref_dump time TRACE.hex CFG REPEATS            (CPU baseline timing)
 //   ref_dump report TRACE.hex CFG PREFIX           (build_report + write_report)
+//   ref_dump sim  TRACE.hex CFG                    (engine::run only, no output files;
+//                                                   the bench.py reference arm)
 //
 // Trace files use the lossless hex-float format "pascal-trace-hex-v1"
 // (one line per request: id arrival(%a) prompt reasoning answering preloaded).
@@ -21,6 +23,7 @@
 //     NMIG (start end)* NDEL delivery* NDIG digest*
 // (fields of metrics::RequestRecord, proj/include/pascalsim/metrics.hpp:15-28)
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -180,6 +183,13 @@ int main(int argc, char** argv) {
             }
             std::printf("{\"capacity\": %ld, \"derive_s\": %.6f, \"run_s\": %.6f, \"reps\": %d}\n",
                         cap, std::chrono::duration<double>(t1 - t0).count(), run_s / reps, reps);
+        } else if (mode == "sim" && argc == 4) {
+            auto t = read_hex_trace(argv[2]);
+            Cfg c = read_cfg(argv[3]);
+            auto recs = engine::run(t, c.rc, c.prof);
+            double last = 0.0;
+            for (const auto& r : recs) last = std::max(last, r.completion);
+            std::printf("%zu %a\n", recs.size(), last);
         } else if (mode == "report" && argc == 5) {
             auto t = read_hex_trace(argv[2]);
             Cfg c = read_cfg(argv[3]);

@@ -27,8 +27,9 @@ ABI_SYMBOLS = (
     "pascal_run_batch", "pascal_last_timing", "pascal_run_dump", "pascal_derive_capacity",
     "pascal_trace_load_hex", "pascal_trace_save_hex", "pascal_trace_from_arrays",
     "pascal_trace_get", "pascal_trace_request_iterations", "pascal_set_device",
-    "pascal_device_available",
+    "pascal_device_available", "pascal_batch_set_groups", "pascal_batch_histograms",
 )
+HIST_BINS = 128
 
 
 class RunConfig(C.Structure):
@@ -143,6 +144,8 @@ def bind(lib: C.CDLL, extensions: bool = True) -> C.CDLL:
         "pascal_trace_request_iterations": (C.c_longlong, [P]),
         "pascal_set_device": (st, [C.c_int]),
         "pascal_device_available": (C.c_int, []),
+        "pascal_batch_set_groups": (st, [P, C.POINTER(C.c_int), C.c_int]),
+        "pascal_batch_histograms": (st, [P, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
     }
     for name, (res, args) in sig.items():
         if not extensions and not hasattr(lib, name):

@@ -276,6 +276,20 @@ class Batch:
         _check(_lib_().pascal_batch_summaries(self._h, out))
         return list(out)
 
+    def set_groups(self, group_of_replica: Sequence[int], n_groups: int) -> None:
+        self.n_groups = n_groups
+        arr = (C.c_int * self.n)(*group_of_replica)
+        _check(_lib_().pascal_batch_set_groups(self._h, arr, n_groups))
+
+    def histograms(self):
+        """(hist[n_groups][HIST_BINS + 2], slo[n_groups][2]) as nested lists."""
+        nb = _lib.HIST_BINS + 2
+        h = (C.c_ulonglong * (self.n_groups * nb))()
+        s = (C.c_ulonglong * (self.n_groups * 2))()
+        _check(_lib_().pascal_batch_histograms(self._h, h, s))
+        return ([list(h[g * nb:(g + 1) * nb]) for g in range(self.n_groups)],
+                [list(s[2 * g:2 * g + 2]) for g in range(self.n_groups)])
+
 
 def run_batch(traces, profiles, cfgs) -> List[_lib.Summary]:
     n, tt, pp, cc = _arrays(traces, profiles, cfgs)

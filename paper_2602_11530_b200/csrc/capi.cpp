@@ -351,6 +351,22 @@ void pascal_batch_free(pascal_batch* b) {
     delete b;
 }
 
+pascal_status pascal_batch_set_groups(pascal_batch* b, const int* group_of_replica,
+                                      int n_groups) {
+    return guarded([&] {
+        need(b && b->b && group_of_replica, "null argument");
+        batch_set_groups(b->b, group_of_replica, n_groups);
+    });
+}
+
+pascal_status pascal_batch_histograms(pascal_batch* b, unsigned long long* hist,
+                                      unsigned long long* slo) {
+    return guarded([&] {
+        need(b && b->b && hist && slo, "null argument");
+        batch_histograms(b->b, hist, slo);
+    });
+}
+
 pascal_status pascal_run_batch(const pascal_trace* const* traces,
                                const pascal_profile* const* profiles,
                                const pascal_run_config* cfgs, size_t count,

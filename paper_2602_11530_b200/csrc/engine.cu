@@ -596,10 +596,13 @@ DEVI void pop_stack(const Rep& R, Adm& A, int s, long long need) {
     }
 }
 
-// Gather one queue into tmp (and optionally demote first). Returns the number
-// of candidates appended at tmp[*nt..]; tracks min/max quanta.
+// Gather one queue (demoting first when Pascal scans the high queue) into
+// cand[nt..] in queue order; quanta go to tmpq for the partition. Returns the
+// min / max quanta of the gathered candidates and how many have quanta 0.
 DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned& qmin,
-                       unsigned& qmax) {
+                       unsigned& qmax, int& zero_q) {
+    unsigned lmin = 0xffffffffu, lmax = 0;
+    int lzero = 0;
     uint2* q = queue_ptr(R, i, low);
     int len = low ? R.s.lo_len[i] : R.s.hi_len[i];
     const bool demote = (R.policy == kPascal) && !low;
@@ -677,14 +680,17 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
             }
             if (h.w > 0) flags |= CF_QPOS;
             int pos = nt + __popc(cm & lanemask_lt());
-            R.tmp[pos] = make_int4((int)e.x, need, h.x, flags);
+            R.cand[pos] = make_int4((int)e.x, need, h.x, flags);
             R.tmpq[pos] = (unsigned)h.w;
+            lmin = min(lmin, (unsigned)h.w);
+            lmax = max(lmax, (unsigned)h.w);
+            lzero += h.w == 0;
         }
-        unsigned qv = cnd ? (unsigned)h.w : 0xffffffffu;
-        qmin = min(qmin, warp_min_u(qv));
-        qmax = max(qmax, warp_max_u(cnd ? (unsigned)h.w : 0u));
         nt += __popc(cm);
     }
+    qmin = warp_min_u(lmin);
+    qmax = warp_max_u(lmax);
+    zero_q = warp_sum(lzero);
     __syncwarp();
     if (lane_id() == 0) {
         if (low) R.s.lo_len[i] = w;
@@ -693,14 +699,13 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
     __syncwarp();
 }
 
-// Stable partition of tmp[s, e) by quanta ascending into cand[s, e)
-// (== sort by (quanta, enqueue_seq) since queues are in seq order).
+// Stable partition of cand[s, e) by quanta ascending (== sort by (quanta,
+// enqueue_seq) since queues are in seq order). Nothing moves when all quanta
+// are equal, the common case.
 DEVI void order_segment(const Rep& R, int s, int e, unsigned qmin, unsigned qmax, bool by_quanta) {
-    if (!by_quanta || qmin >= qmax) {
-        for (int k = s + lane_id(); k < e; k += 32) R.cand[k] = R.tmp[k];
-        __syncwarp();
-        return;
-    }
+    if (!by_quanta || qmin >= qmax) return;
+    for (int k = s + lane_id(); k < e; k += 32) R.tmp[k] = R.cand[k];
+    __syncwarp();
     int out = s;
     unsigned q = qmin;
     while (true) {
@@ -756,11 +761,11 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     const bool classed = pascal;
 
     // ---- gather (+ demotion) and priority order (instance.cpp:113-141)
-    int nt = 0;
+    int nt = 0, z0 = 0, z1 = 0;
     unsigned qmin0 = 0xffffffffu, qmax0 = 0, qmin1 = 0xffffffffu, qmax1 = 0;
-    gather_queue(R, S, i, 0, nt, qmin0, qmax0);
+    gather_queue(R, S, i, 0, nt, qmin0, qmax0, z0);
     int c1 = nt;
-    if (pascal) gather_queue(R, S, i, 1, nt, qmin1, qmax1);
+    if (pascal) gather_queue(R, S, i, 1, nt, qmin1, qmax1, z1);
     const int n = nt;
     S.visits += n;
     const bool by_quanta = R.policy == kRr || pascal;
@@ -771,19 +776,9 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         order_segment(R, 0, n, qmin0, qmax0, by_quanta);
     }
     // k0: first class-0 candidate with quanta > 0 (victims of a class-0
-    // admission form the suffix [k0, n), instance.cpp:158-162)
-    int k0 = c1;
-    if (classed) {
-        for (int base = 0; base < c1; base += 32) {
-            int k = base + lane_id();
-            bool qp = k < c1 && (R.cand[k].w & CF_QPOS);
-            unsigned mk = __ballot_sync(FULL, qp);
-            if (mk) {
-                k0 = base + __ffs(mk) - 1;
-                break;
-            }
-        }
-    }
+    // admission form the suffix [k0, n), instance.cpp:158-162); after the
+    // partition the quanta-0 candidates lead the class-0 block
+    const int k0 = z0;
 
     // ---- admission / controlled preemption (instance.cpp:143-243)
     // Warp-parallel greedy with an exact scalar slow path. Per chunk of 32
@@ -849,8 +844,9 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             const int stop = sm ? __ffs(sm) - 1 : cnt;
             const bool fin = mine && ln < stop;
             if (fin) st = fc ? CS_ADMIT : CS_DENY;
-            const long long taken = warp_sum_ll(fin ? contrib : 0);
-            A.free_ -= taken;
+            // pin at lane stop-1 = admitted need so far (lanes < k contribute 0)
+            const long long taken = __shfl_sync(FULL, pin, max(stop - 1, 0));
+            if (stop > 0) A.free_ -= taken;
             if (__ballot_sync(FULL, fin && fc)) any_admitted = true;
             if (stop >= cnt) break;
             // ---- exact reference step for candidate `stop`
@@ -902,12 +898,13 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         const unsigned wm = __ballot_sync(FULL, wt);
         if (wm && pf == INT_MAX) pf = base + __ffs(wm) - 1;
         bcount += __popc(__ballot_sync(FULL, inb));
-        bkv += warp_sum_ll(inb ? (long long)my.z : 0);
+        bkv += inb ? (long long)my.z : 0;  // lane-local; reduced after the loop
         nsw += __popc(__ballot_sync(FULL, sw));
         nimm += __popc(__ballot_sync(FULL, imm));
         nden += __popc(__ballot_sync(FULL, den));
         __syncwarp();
     }
+    bkv = warp_sum_ll(bkv);
     if (A.free_ < 0) pop_stack(R, A, 0, 0);  // over-capacity repair :235-243
 
     int kind;  // 0 idle, 1 prefill, 2 decode
@@ -959,6 +956,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     // pass B: swap-ins, immediate swap-ins, denials, batch, in candidate order
     long long lsw = log0 + A.ne, limm = lsw + nsw, lden = limm + nimm;
     int bpos = 0;
+    long long mv = 0;
     unsigned* bout = R.batch + (long long)i * R.n;
     for (int base = 0; base < n; base += 32) {
         int k = base + lane_id();
@@ -997,9 +995,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             log_put(R, lden + __popc(dnm & lt), S.now, kLBlock, i, c.x, 0);
         }
         if (inb && kind == 2) bout[bpos + __popc(bm & lt)] = (unsigned)c.x;
-        long long mv = warp_sum_ll((sw || imm) ? (long long)c.z : 0);
-        add_cpu(R, i, -mv);
-        add_gpu(R, S, i, mv);
+        mv += (sw || imm) ? (long long)c.z : 0;  // lane-local; reduced after the loop
         lsw += __popc(swm);
         limm += __popc(imm_m);
         lden += __popc(dnm);
@@ -1013,6 +1009,9 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         }
     }
     S.nlog = log0 + A.ne + nsw + nimm + nden;
+    mv = warp_sum_ll(mv);
+    add_cpu(R, i, -mv);
+    add_gpu(R, S, i, mv);
     __syncwarp();
 
     if (kind == 1) {
@@ -1136,6 +1135,7 @@ DEVI void on_iteration_complete(Rep& R, Scal& S, int i) {
     if (lane_id() == 0) R.s.blen[i] = 0;
     const bool use_quanta = R.policy == kRr || R.policy == kPascal;
     const bool pascal = R.policy == kPascal;
+    const bool logging = (R.flags & kLogEvents) != 0;
     const unsigned* bin = R.batch + (long long)i * R.n;
     S.req_iters += nb;
     for (int base = 0; base < nb; base += 32) {
@@ -1175,9 +1175,11 @@ DEVI void on_iteration_complete(Rep& R, Scal& S, int i) {
             unsigned seg = remaining & (t == 32 ? FULL : ((1u << t) - 1u));
             bool in = (seg >> lane_id()) & 1u;
             // ---- parallel segment: token, quanta, delivery, finish
-            int lines = in ? 1 + (fin ? 1 : 0) + ((!pascal && trans) ? 1 : 0) : 0;
-            int ltot;
-            int lpos = warp_excl_scan(lines, &ltot);
+            int ltot = 0, lpos = 0;
+            if (logging) {
+                int lines = in ? 1 + (fin ? 1 : 0) + ((!pascal && trans) ? 1 : 0) : 0;
+                lpos = warp_excl_scan(lines, &ltot);
+            }
             long long freed = 0;
             if (in) {
                 unsigned mm = m;
@@ -1209,9 +1211,11 @@ DEVI void on_iteration_complete(Rep& R, Scal& S, int i) {
                 if (mm != m) R.meta[idx] = mm;
             }
             S.nlog += ltot;
-            long long fr = warp_sum_ll(freed);
-            if (fr) add_gpu(R, S, i, -fr);
-            S.done += __popc(__ballot_sync(FULL, in && fin));
+            const unsigned fm = __ballot_sync(FULL, in && fin);
+            if (fm) {
+                add_gpu(R, S, i, -warp_sum_ll(freed));
+                S.done += __popc(fm);
+            }
             __syncwarp();
             if (t == 32) break;
             // ---- Pascal phase boundary for lane t, applied in batch order

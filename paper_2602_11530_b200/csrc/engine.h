@@ -184,6 +184,8 @@ PB_HD inline int smem_per_warp(int ni, int n_smem, int c_smem) {
            smem_cand_bytes(c_smem);
 }
 
+constexpr int kHistBins = 128;  // PASCAL_HIST_BINS
+
 // Host entries (engine.cu / metrics.cu). All enqueue on `stream`.
 int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int warps_per_block,
                   int blocks, void* stream);
@@ -193,6 +195,9 @@ int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int warps_
 int launch_capacity(ReplicaDesc* desc, const ReplicaOut* oracle_out, const int* map,
                     const double* fraction, const long long* biggest, long long* echo,
                     int count, void* stream);
+int launch_histograms(const int* rid, const int* group, const RowArrays rows,
+                      const ReplicaOut* out, long long total, int n_groups,
+                      unsigned long long* hist, unsigned long long* slo, void* stream);
 int launch_metrics(const Arena& a, const MetricParams* params, const long long* seg,
                    const int* rid, long long total, int n_rep, RowArrays rows,
                    DevSummary* out, const long long* echo_capacity, void* sort_tmp,

@@ -155,6 +155,8 @@ Batch* batch_create(const std::vector<Job>& jobs);
 void batch_execute(Batch* b);
 void batch_summaries(Batch* b, std::vector<DeviceSummary>& out);
 void batch_free(Batch* b);
+void batch_set_groups(Batch* b, const int* group_of_replica, int n_groups);
+void batch_histograms(Batch* b, unsigned long long* hist, unsigned long long* slo);
 
 struct Timing {
     double derive_ms = 0, engine_ms = 0, metrics_ms = 0, total_ms = 0, h2d_ms = 0, d2h_ms = 0;

@@ -61,28 +61,38 @@ struct Shape {
 };
 
 Shape pick_shape(int reps, int max_ni, int max_n) {
-    int dev = 0, sms = 148, optin = 0;
+    int dev = 0, sms = 148, optin = 0, per_sm_smem = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const int budget = std::max(48 * 1024, optin) - 1024;
+    cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    const int budget = std::max(48 * 1024, optin) - 1024;  // per CTA
+    const int sm_budget = std::max(budget, per_sm_smem - 2048);
+    constexpr int kMaxWarpsPerSm = 16;  // 128 registers per thread
     const char* env = std::getenv("PB_SMEM");
-    const bool allow_smem = !(env && env[0] == '0');
-    Shape sh{};
-    sh.c_smem = std::min(max_n, 1024);
-    sh.n_smem = allow_smem ? max_n : 0;
-    while (sh.n_smem > 0 && pb::smem_per_warp(max_ni, sh.n_smem, sh.c_smem) > budget)
-        sh.n_smem = 0;  // request state does not fit: HBM-resident replicas
-    while (pb::smem_per_warp(max_ni, sh.n_smem, sh.c_smem) > budget && sh.c_smem > 0)
-        sh.c_smem /= 2;
-    if (!allow_smem) sh.c_smem = 0;
-    const int per_warp = pb::smem_per_warp(max_ni, sh.n_smem, sh.c_smem);
-    const int fit = std::max(1, std::min(4, budget / per_warp));
-    sh.wpb = std::max(1, std::min(fit, reps / std::max(1, sms)));
-    const int per_sm = std::max(1, std::min(32 / sh.wpb, (228 * 1024) / (per_warp * sh.wpb)));
-    sh.blocks = std::max(1, std::min((reps + sh.wpb - 1) / sh.wpb, sms * per_sm));
+    const int mode = env ? std::atoi(env) : -1;  // 0: HBM request state, 1: shared, -1: auto
+    const int need_w = std::max(1, std::min(kMaxWarpsPerSm, (reps + sms - 1) / std::max(1, sms)));
+    auto warps_fit = [&](int per_warp) {
+        return std::max(0, std::min(kMaxWarpsPerSm, sm_budget / std::max(1, per_warp)));
+    };
+    // A: request state + heap + candidate scratch in shared memory
+    Shape a{max_n, std::min(max_n, 1024), 0, 0};
+    int pa = pb::smem_per_warp(max_ni, a.n_smem, a.c_smem);
+    bool a_ok = pa <= budget && mode != 0;
+    // B: request state in HBM (L2-resident), small shared candidate scratch
+    Shape b{0, std::min(max_n, 512), 0, 0};
+    while (b.c_smem > 32 && pb::smem_per_warp(max_ni, 0, b.c_smem) * 8 > sm_budget) b.c_smem /= 2;
+    int pbw = pb::smem_per_warp(max_ni, 0, b.c_smem);
+    const bool use_a = a_ok && (mode == 1 || warps_fit(pa) >= std::min(need_w, 4));
+    Shape sh = use_a ? a : b;
+    const int per_warp = use_a ? pa : pbw;
+    const int w = std::max(1, std::min(need_w, warps_fit(per_warp)));
+    sh.wpb = std::max(1, std::min({4, w, budget / per_warp}));
+    const int blocks_per_sm = std::max(1, w / sh.wpb);
+    sh.blocks = std::max(1, std::min((reps + sh.wpb - 1) / sh.wpb, sms * blocks_per_sm));
     return sh;
 }
+
 constexpr long long kMaxReq = (1ll << 26) - 1;  // heap id field
 constexpr int kMaxInst = 512;
 
@@ -169,6 +179,10 @@ public:
     DevBuf<pb::DevSummary> d_sum_;
     DevBuf<char> d_sort_tmp_;
     size_t sort_bytes_ = 0;
+    // sweep histograms
+    int n_groups_ = 0;
+    DevBuf<int> d_group_;
+    DevBuf<unsigned long long> d_hist_, d_slo_hist_;
 
     pb::Arena arena(bool oracle) const;
 };
@@ -439,6 +453,12 @@ void Batch::execute() {
                            d_sum_.p, d_echo_.p, d_sort_tmp_.p, &bytes, st_) != 0)
         throw std::logic_error("metrics launch failed");
     launches += total_req_ > 0 ? 3 : 1;
+    if (n_groups_ > 0) {
+        if (pb::launch_histograms(d_rid_.p, d_group_.p, rows, d_out_.p, total_req_, n_groups_,
+                                  d_hist_.p, d_slo_hist_.p, st_))
+            throw std::logic_error("histogram launch failed");
+        launches += 1;
+    }
     ck(cudaEventRecord(ev_[3], st_), "event");
     ck(cudaEventSynchronize(ev_[3]), "engine sync");
     ck(cudaGetLastError(), "engine");
@@ -538,6 +558,31 @@ Batch* batch_create(const std::vector<Job>& jobs) {
 void batch_execute(Batch* b) { b->execute(); }
 void batch_summaries(Batch* b, std::vector<DeviceSummary>& out) { b->fetch_summaries(out); }
 void batch_free(Batch* b) { delete b; }
+
+void batch_set_groups(Batch* b, const int* group_of_replica, int n_groups) {
+    if (n_groups < 1) throw std::invalid_argument("n_groups must be >= 1");
+    for (int r = 0; r < b->n_rep_; ++r)
+        if (group_of_replica[r] < 0 || group_of_replica[r] >= n_groups)
+            throw std::invalid_argument("group id out of range");
+    b->n_groups_ = n_groups;
+    b->d_group_.ensure(b->n_rep_);
+    b->d_hist_.ensure((size_t)n_groups * (pb::kHistBins + 2));
+    b->d_slo_hist_.ensure((size_t)n_groups * 2);
+    ck(cudaMemcpy(b->d_group_.p, group_of_replica, b->n_rep_ * sizeof(int),
+                  cudaMemcpyHostToDevice),
+       "h2d");
+}
+
+void batch_histograms(Batch* b, unsigned long long* hist, unsigned long long* slo) {
+    if (b->n_groups_ == 0) throw std::invalid_argument("no groups set on this batch");
+    ck(cudaMemcpy(hist, b->d_hist_.p,
+                  sizeof(unsigned long long) * b->n_groups_ * (pb::kHistBins + 2),
+                  cudaMemcpyDeviceToHost),
+       "d2h");
+    ck(cudaMemcpy(slo, b->d_slo_hist_.p, sizeof(unsigned long long) * b->n_groups_ * 2,
+                  cudaMemcpyDeviceToHost),
+       "d2h");
+}
 
 RunOutputs run_single(const Job& job, bool want_records, bool want_log) {
     if (!device_available()) throw std::logic_error("no CUDA device available for the B200 engine");

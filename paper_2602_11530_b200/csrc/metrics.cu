@@ -157,6 +157,38 @@ __global__ void summary_kernel(const MetricParams* params, const ReplicaDesc* de
     if (lane == 0) sum[r] = s;
 }
 
+// Per-group TTFT histogram + SLO counters over all requests of the group's
+// replicas (the sweep's device-side reduction; merged across GPUs by NCCL).
+__global__ void hist_kernel(const int* rid, const int* group, RowArrays rows,
+                            const ReplicaOut* out, long long total, unsigned long long* hist,
+                            unsigned long long* slo) {
+    long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= total) return;
+    const int r = rid[g];
+    if (out[r].status != 0) return;
+    const int grp = group[r];
+    const double t = rows.ttft[g];
+    int bin;
+    if (!(t >= 1e-4)) bin = 0;
+    else if (t >= 1e5) bin = kHistBins + 1;
+    else bin = 1 + min(kHistBins - 1, (int)((log10(t) + 4.0) * (kHistBins / 9.0)));
+    atomicAdd(&hist[(long long)grp * (kHistBins + 2) + bin], 1ull);
+    atomicAdd(&slo[2 * grp], (unsigned long long)rows.slo[g]);
+    atomicAdd(&slo[2 * grp + 1], 1ull);
+}
+
+int launch_histograms(const int* rid, const int* group, const RowArrays rows,
+                      const ReplicaOut* out, long long total, int n_groups,
+                      unsigned long long* hist, unsigned long long* slo, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * n_groups * (kHistBins + 2), st);
+    cudaMemsetAsync(slo, 0, sizeof(unsigned long long) * n_groups * 2, st);
+    if (total > 0)
+        hist_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(rid, group, rows, out, total,
+                                                                     hist, slo);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
 int launch_capacity(ReplicaDesc* desc, const ReplicaOut* oracle_out, const int* map,
                     const double* fraction, const long long* biggest, long long* echo,
                     int count, void* stream) {
