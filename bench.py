@@ -46,13 +46,18 @@ ACC_CHAT = ("uniform:64:512", "hist:256=0.35,512=0.30,768=0.20,1024=0.10,1536=0.
             "uniform:1024:4096")
 ACC_HEAVY = ("uniform:64:512", "uniform:2048:4608", "uniform:128:512")
 
+# C5 bench slice: rates k >= 3 (lambda >= 2 req/s, the range SURVEY.md §6.3
+# measured). At lambda < 2 and capacity 0.5 Pascal replicas enter an
+# evict/swap-in thrash regime (the reference ran > 39 CPU-minutes on one).
+C5_IDS = [r for r in range(4096 * 64) if sweep.replica_params(r)[1] >= 3]
+
 WORKLOADS = {
     # label: (description, default replicas per GPU)
     "c2": ("C2: chat preset, 2000 req, lambda 12, 4 instances, capacity_fraction 0.3, pascal",
            296),
     "c1": ("C1: chat preset, 64 req, lambda 12, 1 instance, capacity_fraction 0.5, pascal", 4736),
-    "c5": ("C5 slice: acceptance mixed 256 req, 4 instances, cap 0.5, lambda 2^(k/3), "
-           "4 policies", 4736),
+    "c5": ("C5 slice: acceptance mixed 256 req, 4 instances, cap 0.5, lambda 2^(k/3) k=3..15, "
+           "4 policies, seeds 0..", 4736),
 }
 
 
@@ -75,7 +80,7 @@ def replica_specs(workload, rank, per_gpu):
             out.append(({"gen": [64, 12.0, *CHAT, 1 + g, False]},
                         dict(policy="pascal", instance_count=1, capacity_fraction=0.5), {}))
         else:
-            out.append(sweep.replica_recipe(g))
+            out.append(sweep.replica_recipe(C5_IDS[g]))
     return out
 
 

@@ -199,6 +199,8 @@ struct Rep {
 };
 
 struct Scal {
+    HeapEnt* heap;        // shared-memory heap, or the HBM heap after a spill
+    long long heap_slots;  // usable slots (1-based: entries 1..heap_slots-1)
     double now;
     unsigned long long evseq;
     unsigned enq;
@@ -245,9 +247,17 @@ DEVI void heap_push(const Rep& R, Scal& S, double t, unsigned kind, unsigned id)
         return;
     }
     unsigned long long key = ((++S.evseq) << 29) | ((unsigned long long)kind << 26) | id;
+    if (S.hn + 1 >= S.heap_slots && S.heap != R.heap) {
+        // shared-memory heap full: move it to the HBM heap (sized for every
+        // pending event) and stay there
+        for (int k = 1 + lane_id(); k <= S.hn; k += 32) R.heap[k] = S.heap[k];
+        __syncwarp();
+        S.heap = R.heap;
+        S.heap_slots = (long long)R.n + R.ni + 2;
+    }
     int pos = ++S.hn;
     if (lane_id() == 0) {
-        HeapEnt* h = R.heap;
+        HeapEnt* h = S.heap;
         while (pos > 1) {
             int p = pos >> 1;
             HeapEnt pe = h[p];
@@ -264,7 +274,7 @@ DEVI HeapEnt heap_pop(const Rep& R, Scal& S) {
     HeapEnt top;
     int n = S.hn;
     if (lane_id() == 0) {
-        HeapEnt* h = R.heap;
+        HeapEnt* h = S.heap;
         top = h[1];
         HeapEnt last = h[n];
         int m = n - 1;
@@ -607,21 +617,45 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
     int len = low ? R.s.lo_len[i] : R.s.hi_len[i];
     const bool demote = (R.policy == kPascal) && !low;
     int w = 0;
+    // Two-deep software pipeline: while chunk c is processed, the request
+    // state of chunk c+1 and the queue entries of chunk c+2 are in flight.
+    // Safe because a request has at most one entry in a high queue (appended
+    // once, at arrival) and the low-queue scan writes no request state.
+    const int ln = lane_id();
+    uint2 e_c = make_uint2(0, 0), e_n = make_uint2(0, 0);
+    int4 h_c = make_int4(0, 0, 0, 0);
+    unsigned m_c = 0;
+    if (ln < len) {
+        e_c = q[ln];
+        h_c = R.hot[e_c.x];
+        m_c = R.meta[e_c.x];
+    }
+    if (32 + ln < len) e_n = q[32 + ln];
     for (int base = 0; base < len; base += 32) {
-        int k = base + lane_id();
+        int k = base + ln;
+        int4 h_n = make_int4(0, 0, 0, 0);
+        unsigned m_n = 0;
+        uint2 e_nn = make_uint2(0, 0);
+        if (k + 32 < len) {
+            h_n = R.hot[e_n.x];
+            m_n = R.meta[e_n.x];
+        }
+        if (k + 64 < len) e_nn = q[k + 64];
         bool live = false, dem = false, cnd = false;
-        uint2 e = make_uint2(0, 0);
-        int4 h = make_int4(0, 0, 0, 0);
+        uint2 e = e_c;
+        int4 h = h_c;
         unsigned m = 0;
         if (k < len) {
-            e = q[k];
-            h = R.hot[e.x];
             live = (unsigned)h.z == e.y;
             if (live) {
-                m = R.meta[e.x];
+                m = m_c;
                 dem = demote && (long long)h.x > R.demotion;  // strict, instance.cpp:44
             }
         }
+        e_c = e_n;
+        h_c = h_n;
+        m_c = m_n;
+        e_n = e_nn;
         // --- demotion (instance.cpp:39-57): new seqs in queue order, appended
         // to the low queue; logged "demote" in that order (engine.cpp:196-197).
         unsigned dm = __ballot_sync(FULL, dem);
@@ -958,15 +992,30 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     int bpos = 0;
     long long mv = 0;
     unsigned* bout = R.batch + (long long)i * R.n;
+    // pipelined: the blocked totals of the next chunk's denials are loaded
+    // while this chunk is applied (a request is a candidate at most once)
+    int4 c_n = make_int4(0, 0, 0, 0);
+    unsigned char st_n = 0;
+    double bl_n = 0.0;
+    if (lane_id() < n) {
+        c_n = R.cand[lane_id()];
+        st_n = R.cstat[lane_id()];
+        if (st_n == CS_DENY) bl_n = R.blocked[c_n.x];
+    }
     for (int base = 0; base < n; base += 32) {
         int k = base + lane_id();
+        const int4 c = c_n;
+        const unsigned char st_c = st_n;
+        const double bl = bl_n;
+        if (k + 32 < n) {
+            c_n = R.cand[k + 32];
+            st_n = R.cstat[k + 32];
+            bl_n = st_n == CS_DENY ? R.blocked[c_n.x] : 0.0;
+        }
         bool adm = false, den = false, inb = false, sw = false, imm = false;
-        int4 c = make_int4(0, 0, 0, 0);
         if (k < n) {
-            c = R.cand[k];
-            unsigned char st = R.cstat[k];
-            adm = st == CS_ADMIT;
-            den = st == CS_DENY;
+            adm = st_c == CS_ADMIT;
+            den = st_c == CS_DENY;
         }
         double sd = 0.0;
         if (adm && !(c.w & CF_WAIT)) {
@@ -991,7 +1040,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             log_put(R, limm + __popc(imm_m & lt), S.now, kLSwapIn, i, c.x, 0);
         }
         if (den) {
-            R.blocked[c.x] = __dadd_rn(R.blocked[c.x], dur);
+            R.blocked[c.x] = __dadd_rn(bl, dur);
             log_put(R, lden + __popc(dnm & lt), S.now, kLBlock, i, c.x, 0);
         }
         if (inb && kind == 2) bout[bpos + __popc(bm & lt)] = (unsigned)c.x;
@@ -1138,23 +1187,42 @@ DEVI void on_iteration_complete(Rep& R, Scal& S, int i) {
     const bool logging = (R.flags & kLogEvents) != 0;
     const unsigned* bin = R.batch + (long long)i * R.n;
     S.req_iters += nb;
+    // two-deep pipeline as in gather_queue: a request is in a batch once, and
+    // a member's phase boundary only touches its own state
+    const int ln = lane_id();
+    int idx_c = 0, idx_n = 0;
+    int4 h_c = make_int4(0, 0, 0, 0), sp_c = make_int4(0, 0, 0, 0);
+    unsigned m_c = 0;
+    int qu_c = 0;
+    if (ln < nb) {
+        idx_c = (int)bin[ln];
+        h_c = R.hot[idx_c];
+        m_c = R.meta[idx_c];
+        sp_c = R.spec[idx_c];
+        qu_c = use_quanta ? R.qused[idx_c] : 0;
+    }
+    if (32 + ln < nb) idx_n = (int)bin[32 + ln];
     for (int base = 0; base < nb; base += 32) {
-        int k = base + lane_id();
+        int k = base + ln;
         bool act = k < nb;
-        int idx = 0;
-        int4 h = make_int4(0, 0, 0, 0), sp = make_int4(0, 0, 0, 0);
-        unsigned m = 0;
-        int qu = 0;
+        int idx = idx_c;
+        int4 h = h_c, sp = sp_c;
+        unsigned m = m_c;
+        int qu = qu_c;
+        if (k + 32 < nb) {
+            idx_c = idx_n;
+            h_c = R.hot[idx_n];
+            m_c = R.meta[idx_n];
+            sp_c = R.spec[idx_n];
+            qu_c = use_quanta ? R.qused[idx_n] : 0;
+        }
+        if (k + 64 < nb) idx_n = (int)bin[k + 64];
         bool fresh_lost = false;
         if (act) {
-            idx = (int)bin[k];
-            h = R.hot[idx];
-            m = R.meta[idx];
-            sp = R.spec[idx];
             h.y += 1;
             h.x += 1;
             if (use_quanta) {
-                qu = R.qused[idx] + 1;
+                qu = qu + 1;
                 if ((long long)qu >= R.quantum) {
                     qu = 0;
                     h.w += 1;
@@ -1277,7 +1345,8 @@ DEVI void on_transfer_complete(Rep& R, Scal& S, int idx) {
 }
 
 // ------------------------------------------------------------ the replica
-DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem, int c_smem) {
+DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem, int c_smem,
+                      int h_slots) {
     const ReplicaDesc d = a.desc[r];
     Rep R;
     R.n = d.n;
@@ -1345,8 +1414,10 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
         R.aoff = const_cast<int*>(a.aoff32) + g;
     }
     sp += smem_req_bytes(n_smem);
-    if (resident) R.heap = reinterpret_cast<HeapEnt*>(sp);
-    sp += smem_heap_bytes(n_smem, max_ni);
+    HeapEnt* sheap = reinterpret_cast<HeapEnt*>(sp);
+    const long long sheap_slots = resident ? (long long)n_smem + max_ni + 2 : h_slots;
+    if (resident) R.heap = sheap;  // fits every pending event
+    sp += smem_heap_bytes(n_smem, max_ni, h_slots);
     R.c_smem = c_smem;
     R.s_cand = reinterpret_cast<int4*>(sp);
     R.s_tmp = R.s_cand + c_smem;
@@ -1383,6 +1454,8 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     __syncwarp();
 
     Scal S;
+    S.heap = sheap;
+    S.heap_slots = sheap_slots;
     S.now = 0.0;
     S.evseq = (unsigned long long)R.n;  // arrivals hold seqs 1..n (engine.cpp:384-389)
     S.enq = 0;
@@ -1404,7 +1477,7 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
         HeapEnt top;
         top.t = 0.0;
         top.key = 0;
-        if (has_ev) top = R.heap[1];
+        if (has_ev) top = S.heap[1];
         // arrivals carry seqs 1..n, below every dynamic event seq
         bool take_arr = has_arr && (!has_ev || !(top.t < ta));
         double et;
@@ -1458,30 +1531,41 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(128) sched_kernel(Arena a, int max_ni, int n_smem, int c_smem) {
+// MINB = 1: latency shape (few warps per SM, registers unconstrained);
+// MINB = 4: throughput shape (16 warps per SM, <= 128 registers per thread).
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) sched_kernel(Arena a, int max_ni, int n_smem, int c_smem,
+                                                          int h_slots) {
     extern __shared__ __align__(16) char smem_raw[];
     const int warp = threadIdx.x >> 5;
-    char* smem = smem_raw + (size_t)warp * smem_per_warp(max_ni, n_smem, c_smem);
+    char* smem = smem_raw + (size_t)warp * smem_per_warp(max_ni, n_smem, c_smem, h_slots);
     while (true) {
         int r = 0;
         if (lane_id() == 0) r = atomicAdd(a.work, 1);
         r = __shfl_sync(FULL, r, 0);
         if (r >= a.n_rep) break;
-        run_replica(a, r, smem, max_ni, n_smem, c_smem);
+        run_replica(a, r, smem, max_ni, n_smem, c_smem, h_slots);
     }
 }
 
-int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int warps_per_block,
-                  int blocks, void* stream) {
-    if (warps_per_block < 1 || warps_per_block > 4) return 1;
-    size_t smem = (size_t)warps_per_block * smem_per_warp(max_ni, n_smem, c_smem);
+int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots,
+                  int warps_per_block, int blocks, void* stream) {
+    if (warps_per_block < 1 || warps_per_block > 4 || h_slots < 2) return 1;
+    const size_t smem = (size_t)warps_per_block * smem_per_warp(max_ni, n_smem, c_smem, h_slots);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // the unconstrained variant uses ~248 registers (8 warps per SM); more
+    // warps per SM -> the 128-register variant
+    const bool dense = (long long)blocks * warps_per_block > 8ll * sms;
+    auto kern = dense ? sched_kernel<4> : sched_kernel<1>;
     if (smem > 48 * 1024) {
-        if (cudaFuncSetAttribute(sched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess)
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
             return 2;
     }
-    sched_kernel<<<blocks, warps_per_block * 32, smem, (cudaStream_t)stream>>>(a, max_ni, n_smem,
-                                                                               c_smem);
+    kern<<<blocks, warps_per_block * 32, smem, (cudaStream_t)stream>>>(a, max_ni, n_smem, c_smem,
+                                                                       h_slots);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

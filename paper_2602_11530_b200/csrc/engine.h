@@ -177,18 +177,24 @@ struct RowArrays {
 // HBM; plans with more queued requests than c_smem use the HBM scratch.
 PB_HD inline int smem_inst_bytes(int ni) { return ((ni * 64 + 16) + 15) / 16 * 16; }
 PB_HD inline int smem_req_bytes(int n_smem) { return (n_smem * 60 + 15) / 16 * 16; }
-PB_HD inline int smem_heap_bytes(int n_smem, int ni) { return n_smem ? (n_smem + ni + 2) * 16 : 0; }
+// Shared-memory event heap: sized for every pending event of a resident
+// replica; HBM-resident replicas start with h_slots slots (default 128) and
+// move their heap to HBM if it ever grows past them.
+constexpr int kSmemHeapSlots = 128;
+PB_HD inline int smem_heap_bytes(int n_smem, int ni, int h_slots = kSmemHeapSlots) {
+    return n_smem ? (n_smem + ni + 2) * 16 : h_slots * 16;
+}
 PB_HD inline int smem_cand_bytes(int c_smem) { return (c_smem * 37 + 15) / 16 * 16; }
-PB_HD inline int smem_per_warp(int ni, int n_smem, int c_smem) {
-    return smem_inst_bytes(ni) + smem_req_bytes(n_smem) + smem_heap_bytes(n_smem, ni) +
+PB_HD inline int smem_per_warp(int ni, int n_smem, int c_smem, int h_slots = kSmemHeapSlots) {
+    return smem_inst_bytes(ni) + smem_req_bytes(n_smem) + smem_heap_bytes(n_smem, ni, h_slots) +
            smem_cand_bytes(c_smem);
 }
 
 constexpr int kHistBins = 128;  // PASCAL_HIST_BINS
 
 // Host entries (engine.cu / metrics.cu). All enqueue on `stream`.
-int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int warps_per_block,
-                  int blocks, void* stream);
+int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots,
+                  int warps_per_block, int blocks, void* stream);
 // capacity = max(ceil(fraction * peak / ni), biggest) for the replicas listed
 // in `map` (derive_capacity, proj/src/engine.cpp:466-470); writes echo[r] and,
 // unless the replica runs the oracle policy, desc[r].capacity.

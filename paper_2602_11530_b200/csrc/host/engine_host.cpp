@@ -57,7 +57,7 @@ struct DevBuf {
 // replicas -> one warp per CTA so they spread over all SMs; many -> up to four
 // per CTA, as many as the shared-memory budget allows.
 struct Shape {
-    int n_smem, c_smem, wpb, blocks;
+    int n_smem, c_smem, wpb, blocks, h_slots;
 };
 
 Shape pick_shape(int reps, int max_ni, int max_n) {
@@ -71,18 +71,21 @@ Shape pick_shape(int reps, int max_ni, int max_n) {
     constexpr int kMaxWarpsPerSm = 16;  // 128 registers per thread
     const char* env = std::getenv("PB_SMEM");
     const int mode = env ? std::atoi(env) : -1;  // 0: HBM request state, 1: shared, -1: auto
+    const char* henv = std::getenv("PB_SMEM_HEAP");  // test hook: tiny heap forces HBM spills
+    const int h_slots = henv ? std::max(2, std::atoi(henv)) : pb::kSmemHeapSlots;
     const int need_w = std::max(1, std::min(kMaxWarpsPerSm, (reps + sms - 1) / std::max(1, sms)));
     auto warps_fit = [&](int per_warp) {
         return std::max(0, std::min(kMaxWarpsPerSm, sm_budget / std::max(1, per_warp)));
     };
     // A: request state + heap + candidate scratch in shared memory
-    Shape a{max_n, std::min(max_n, 1024), 0, 0};
-    int pa = pb::smem_per_warp(max_ni, a.n_smem, a.c_smem);
+    Shape a{max_n, std::min(max_n, 1024), 0, 0, h_slots};
+    int pa = pb::smem_per_warp(max_ni, a.n_smem, a.c_smem, h_slots);
     bool a_ok = pa <= budget && mode != 0;
     // B: request state in HBM (L2-resident), small shared candidate scratch
-    Shape b{0, std::min(max_n, 512), 0, 0};
-    while (b.c_smem > 32 && pb::smem_per_warp(max_ni, 0, b.c_smem) * 8 > sm_budget) b.c_smem /= 2;
-    int pbw = pb::smem_per_warp(max_ni, 0, b.c_smem);
+    Shape b{0, std::min(max_n, 512), 0, 0, h_slots};
+    while (b.c_smem > 32 && pb::smem_per_warp(max_ni, 0, b.c_smem, h_slots) * 8 > sm_budget)
+        b.c_smem /= 2;
+    int pbw = pb::smem_per_warp(max_ni, 0, b.c_smem, h_slots);
     const bool use_a = a_ok && (mode == 1 || warps_fit(pa) >= std::min(need_w, 4));
     Shape sh = use_a ? a : b;
     const int per_warp = use_a ? pa : pbw;
@@ -424,7 +427,8 @@ void Batch::execute() {
     Timing& tm = g_timing;
     auto launch = [&](const pb::Arena& ar, int reps, int max_n) {
         const Shape sh = pick_shape(reps, max_ni_, max_n);
-        return pb::launch_engine(ar, max_ni_, sh.n_smem, sh.c_smem, sh.wpb, sh.blocks, st_);
+        return pb::launch_engine(ar, max_ni_, sh.n_smem, sh.c_smem, sh.h_slots, sh.wpb, sh.blocks,
+                                 st_);
     };
     int launches = 0;
     ck(cudaEventRecord(ev_[0], st_), "event");

@@ -73,3 +73,22 @@ def test_run_batch_end_to_end_and_histograms():
     assert sum(v for v, _ in slo) == sum(s.slo_violations for s in summ)
     t = pb.last_timing()
     assert t.engine_ms > 0 and t.kernel_launches >= 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"PB_SMEM": "0"}, {"PB_SMEM": "0", "PB_SMEM_HEAP": "3"},
+                                 {"PB_SMEM": "1"}])
+def test_launch_shapes_are_bit_exact(env, monkeypatch):
+    """Request state in HBM (throughput shape), a 3-slot shared heap that
+    must spill to HBM, and full shared-memory residency all give the
+    reference's summaries."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cases = [c for c in SMALL if c["size"] != "tiny"]
+    traces = [build_trace(c["trace"]) for c in cases]
+    b = pb.Batch(traces, [make_profile(c) for c in cases], [make_cfg(c) for c in cases])
+    b.execute()
+    bad = [c["name"] for c, s in zip(cases, b.summaries())
+           if s.status != 0 or hashlib.sha256(summary_text(c, s)).hexdigest() !=
+           GOLD[c["name"]]["report"]["summary.txt"][0]]
+    assert not bad, bad
