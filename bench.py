@@ -172,9 +172,10 @@ def find_cpu_ref():
     return port, "port"
 
 
-def cpu_time_replicas(specs, procs, tmp):
+def cpu_time_replicas(specs, procs, tmp, outputs=None):
     """Run the CPU reference on `specs` with `procs` parallel processes; returns
-    (wall seconds, request-iterations)."""
+    (wall seconds, request-iterations). With `outputs` (a list), each replica's
+    (ttft_p99, slo_violation_rate, ttft_mean) from the reference is appended."""
     import paper_2602_11530_b200 as pb
     from cases import cfg_text
     from harness import build_trace
@@ -193,13 +194,21 @@ def cpu_time_replicas(specs, procs, tmp):
         jobs.append([exe, "sim", hexp, cfgp])
     t0 = time.perf_counter()
     running = []
+    done = []
     for j in jobs:
         while len(running) >= procs:
-            running.pop(0).wait()
-        running.append(subprocess.Popen(j, stdout=subprocess.DEVNULL))
+            done.append(running.pop(0))
+            done[-1].wait()
+        running.append(subprocess.Popen(j, stdout=subprocess.PIPE, text=True))
     for p in running:
         p.wait()
-    return time.perf_counter() - t0, units
+        done.append(p)
+    dt = time.perf_counter() - t0
+    if outputs is not None:
+        for p in done:
+            f = p.stdout.read().split()
+            outputs.append(tuple(float.fromhex(x) for x in f[1:4]))
+    return dt, units
 
 
 def run_reference(args, rank, world):
@@ -371,13 +380,23 @@ def main():
     hist_all = ghist.sum(0).tolist()
 
     cpu = None
+    parity = None
     if not args.no_cpu_baseline and world == 1:
         exe, kind = find_cpu_ref()
+        outs = []
         with tempfile.TemporaryDirectory() as tmp:
-            dt, u = cpu_time_replicas(specs[:1], 1, tmp)
+            dt, u = cpu_time_replicas(specs[:1], 1, tmp, outs)
         cpu = {"value": u / dt, "unit": UNIT, "cores": 1, "kind": kind,
                "sample": f"1 whole {args.workload} replica (seed 1), engine::run incl. capacity "
                          f"pre-run, single thread"}
+        p99_ref, slo_ref, mean_ref = outs[0]
+        s0 = summ[0]
+        parity = {"replica": 0, "ttft_p99_gpu": s0.ttft_p99, "ttft_p99_cpu_ref": p99_ref,
+                  "slo_violation_rate_gpu": s0.slo_violation_rate,
+                  "slo_violation_rate_cpu_ref": slo_ref, "ttft_mean_gpu": s0.ttft_mean,
+                  "ttft_mean_cpu_ref": mean_ref,
+                  "bit_exact": (s0.ttft_p99, s0.slo_violation_rate, s0.ttft_mean) ==
+                               (p99_ref, slo_ref, mean_ref)}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -397,6 +416,7 @@ def main():
                      "algorithmic_bytes_per_launch": alg,
                      "kernel_ms": ms_engine},
         "cpu_baseline": cpu,
+        "parity_vs_cpu_ref": parity,
         "clocks": clk.summary(),
         "results": {"replicas_all_ranks": len(p99),
                     "ttft_p99_median_over_replicas": p99[len(p99) // 2],

@@ -9,6 +9,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 #include <time.h>
 
 #include "pascal_oracle.h"
@@ -126,10 +127,27 @@ int main(int argc, char** argv) {
             fprintf(stderr, "oracle_dump: %s\n", err);
             return 1;
         }
-        double last = 0.0;
-        for (long k = 0; k < n; ++k)
-            if (recs[k].completion > last) last = recs[k].completion;
-        printf("%ld %a\n", n, last);
+        /* P99 TTFT (nearest rank), SLO-violation rate, mean TTFT (metrics.cpp:115-153) */
+        double* tt = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+        long viol = 0;
+        for (long k = 0; k < n; ++k) {
+            tt[k] = recs[k].first_answer_delivery - recs[k].arrival;
+            if (po_qoe(&recs[k], c.target_tpot) < c.qoe_threshold) ++viol;
+        }
+        for (long a = 1; a < n; ++a) { /* insertion sort: small n, test infrastructure */
+            double x = tt[a];
+            long b = a - 1;
+            while (b >= 0 && tt[b] > x) { tt[b + 1] = tt[b]; --b; }
+            tt[b + 1] = x;
+        }
+        double sum = 0.0;
+        for (long k = 0; k < n; ++k) sum += tt[k];
+        long rank = n ? (long)ceil(0.99 * (double)n) : 1;
+        if (rank < 1) rank = 1;
+        if (rank > n) rank = n;
+        printf("%ld %a %a %a\n", n, n ? tt[rank - 1] : 0.0, n ? (double)viol / (double)n : 0.0,
+               n ? sum / (double)n : 0.0);
+        free(tt);
         po_records_free(recs, n);
     } else if (!strcmp(argv[1], "capacity")) {
         long cap = 0;

@@ -187,9 +187,10 @@ int main(int argc, char** argv) {
             auto t = read_hex_trace(argv[2]);
             Cfg c = read_cfg(argv[3]);
             auto recs = engine::run(t, c.rc, c.prof);
-            double last = 0.0;
-            for (const auto& r : recs) last = std::max(last, r.completion);
-            std::printf("%zu %a\n", recs.size(), last);
+            auto rep = metrics::build_report(recs, c.rc.target_tpot, c.rc.qoe_threshold,
+                                             c.rc.ttfat_target);
+            std::printf("%zu %a %a %a\n", recs.size(), rep.ttft_p99, rep.slo_violation_rate,
+                        rep.ttft_mean);
         } else if (mode == "report" && argc == 5) {
             auto t = read_hex_trace(argv[2]);
             Cfg c = read_cfg(argv[3]);

@@ -1243,10 +1243,12 @@ DEVI void on_iteration_complete(Rep& R, Scal& S, int i) {
             unsigned seg = remaining & (t == 32 ? FULL : ((1u << t) - 1u));
             bool in = (seg >> lane_id()) & 1u;
             // ---- parallel segment: token, quanta, delivery, finish
-            int ltot = 0, lpos = 0;
+            int ltot, lpos = 0;
             if (logging) {
                 int lines = in ? 1 + (fin ? 1 : 0) + ((!pascal && trans) ? 1 : 0) : 0;
                 lpos = warp_excl_scan(lines, &ltot);
+            } else {  // keep the line count exact (sizes a later logged run)
+                ltot = __popc(seg) + __popc(__ballot_sync(FULL, in && (fin || (!pascal && trans))));
             }
             long long freed = 0;
             if (in) {

@@ -590,8 +590,8 @@ void batch_histograms(Batch* b, unsigned long long* hist, unsigned long long* sl
 
 RunOutputs run_single(const Job& job, bool want_records, bool want_log) {
     if (!device_available()) throw std::logic_error("no CUDA device available for the B200 engine");
-    long long cap = want_log ? std::max<long long>(1024, 4 * request_iterations(*job.trace) +
-                                                             16 * (long long)job.trace->size())
+    long long cap = want_log ? std::max<long long>(1024, 8 * request_iterations(*job.trace) +
+                                                             64 * (long long)job.trace->size())
                              : 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         Batch b({job});
