@@ -28,6 +28,8 @@ typedef struct {
     long long answer_tokens;
     long long events, plans, candidate_visits, health_checks;
     long long slo_violations;
+    long long admission_rounds;    /* warp-parallel admission rounds */
+    long long admission_slow_steps; /* candidates decided by the exact scalar step */
     int status;                    /* pascal_status of this replica */
     int pad;
 } pascal_summary;

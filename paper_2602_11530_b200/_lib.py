@@ -64,6 +64,7 @@ class Summary(C.Structure):
         ("events", C.c_longlong), ("plans", C.c_longlong),
         ("candidate_visits", C.c_longlong), ("health_checks", C.c_longlong),
         ("slo_violations", C.c_longlong),
+        ("admission_rounds", C.c_longlong), ("admission_slow_steps", C.c_longlong),
         ("status", C.c_int), ("pad", C.c_int),
     ]
 

@@ -165,11 +165,7 @@ struct Rep {
     const double* arrival;
     int4* spec;
     int* aoff;  // answer-slot offset relative to dig / del
-    int4* hot;
-    unsigned* meta;
-    int* qused;
-    int* ndel;
-    int* cursor;
+    ReqState* rs;
     double* blocked;
     RecOut* rec;
     double* dig;  // this replica's digest arena
@@ -209,7 +205,7 @@ struct Scal {
     int done;
     int status;
     long long gpu_total, peak, nlog;
-    long long events, plans, visits, req_iters, ans_tokens, health;
+    long long events, plans, visits, req_iters, ans_tokens, health, adm_rounds, adm_slow;
 };
 
 DEVI uint2* queue_ptr(const Rep& R, int i, int low) {
@@ -318,11 +314,14 @@ DEVI void queue_compact(const Rep& R, int i, int low) {
         uint2 e = make_uint2(0, 0);
         if (k < len) {
             e = q[k];
-            live = (unsigned)R.hot[e.x].z == e.y;
+            live = (unsigned)R.rs[e.x].h.z == e.y;
         }
         unsigned mk = __ballot_sync(FULL, live);
         __syncwarp();
-        if (live) q[w + __popc(mk & lanemask_lt())] = e;
+        {
+            const int dst = w + __popc(mk & lanemask_lt());
+            if (live && dst != k) q[dst] = e;
+        }
         w += __popc(mk);
     }
     __syncwarp();
@@ -342,12 +341,12 @@ DEVI void enqueue(const Rep& R, Scal& S, int i, int idx, bool high) {
     }
     unsigned seq = ++S.enq;
     if (lane_id() == 0) {
-        int4 h = R.hot[idx];
+        int4 h = R.rs[idx].h;
         h.z = (int)seq;
-        R.hot[idx] = h;
-        unsigned m = R.meta[idx];
+        R.rs[idx].h = h;
+        unsigned m = R.rs[idx].meta;
         m = m_set_owner(m_set_qlow(m, !high), i);
-        R.meta[idx] = m;
+        R.rs[idx].meta = m;
         queue_ptr(R, i, high ? 0 : 1)[len] = make_uint2((unsigned)idx, seq);
         if (high) {
             R.s.hi_len[i] = len + 1;
@@ -363,9 +362,9 @@ DEVI void enqueue(const Rep& R, Scal& S, int i, int idx, bool high) {
 
 // engine.cpp:122-126 (lane 0 only; caller syncs)
 DEVI void dequeue_lane(const Rep& R, int idx, int owner, unsigned m, int quanta) {
-    int4 h = R.hot[idx];
+    int4 h = R.rs[idx].h;
     h.z = 0;
-    R.hot[idx] = h;
+    R.rs[idx].h = h;
     if (m_qlow(m)) {
         atomicSub(&R.s.lcount[owner], 1);
         if (quanta == 0) atomicSub(&R.s.afresh[owner], 1);
@@ -378,15 +377,15 @@ DEVI void dequeue_lane(const Rep& R, int idx, int owner, unsigned m, int quanta)
 // PacerState::healthy (instance.cpp:22-33) with a monotone cursor: `now`
 // never decreases, so the count of digests <= now only grows.
 DEVI bool pacer_healthy(const Rep& R, Scal& S, int idx, int answering) {
-    int nd = R.ndel[idx];
+    int nd = R.rs[idx].ndel;
     if (nd == 0) return true;
     const double* d = R.dig + R.aoff[idx];
     double t0 = d[0];
     long long expected = 1 + (long long)floor(__ddiv_rn(__dsub_rn(S.now, t0), R.tpot));
     if (expected > answering) expected = answering;
-    int c = R.cursor[idx];
+    int c = R.rs[idx].cursor;
     while (c < nd && d[c] <= S.now) ++c;
-    R.cursor[idx] = c;
+    R.rs[idx].cursor = c;
     return (long long)c >= expected - R.slack;
 }
 
@@ -404,9 +403,9 @@ DEVI void compute_health(const Rep& R, Scal& S) {
             bool chk = false;
             if (k < len) {
                 uint2 e = q[k];
-                int4 h = R.hot[e.x];
+                int4 h = R.rs[e.x].h;
                 if ((unsigned)h.z == e.y) {
-                    unsigned m = R.meta[e.x];
+                    unsigned m = R.rs[e.x].meta;
                     if (m_phase(m) == PH_ANSWER) {
                         chk = true;
                         bad = !pacer_healthy(R, S, (int)e.x, R.spec[e.x].z);
@@ -486,8 +485,8 @@ DEVI void note_peak(Scal& S) {  // engine.cpp:75-79
 // engine.cpp:159-190 (Pascal branch; the caller has already set phase,
 // reasoning_end and logged "transition").
 DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
-    unsigned m = R.meta[idx];
-    int4 h = R.hot[idx];
+    unsigned m = R.rs[idx].meta;
+    int4 h = R.rs[idx].h;
     int cur = m_owner(m);
     if (lane_id() == 0) dequeue_lane(R, idx, cur, m, h.w);
     __syncwarp();
@@ -506,10 +505,10 @@ DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
     }
     if (!migrate) {
         if (lane_id() == 0) {
-            R.qused[idx] = 0;
-            int4 hh = R.hot[idx];
+            R.rs[idx].qused = 0;
+            int4 hh = R.rs[idx].h;
             hh.w = 0;
-            R.hot[idx] = hh;
+            R.rs[idx].h = hh;
         }
         __syncwarp();
         enqueue(R, S, cur, idx, false);
@@ -525,7 +524,7 @@ DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
     double fin = __dadd_rn(start, dur);
     if (lane_id() == 0) {
         R.s.link[target] = fin;
-        R.meta[idx] = m_set_owner(m_set_loc(m, LOC_TRANSIT), target);
+        R.rs[idx].meta = m_set_owner(m_set_loc(m, LOC_TRANSIT), target);
         RecOut* rc = &R.rec[idx];
         rc->mig_start = S.now;
         rc->mig_end = fin;
@@ -539,13 +538,13 @@ DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
 // Shared by the R == 0 path of prefill completion: a single answer delivery
 // (PacerState::on_delivery, instance.cpp:10-20 + engine.cpp:148-156).
 DEVI void deliver_lane(const Rep& R, double now, int idx, double iter_start) {
-    int nd = R.ndel[idx];
+    int nd = R.rs[idx].ndel;
     const int off = R.aoff[idx];
     double* d = R.dig + off;
     double v = nd == 0 ? now : dmax(now, __dadd_rn(d[nd - 1], R.tpot));
     d[nd] = v;
     if (R.flags & kRecordDeliv) R.del[off + nd] = now;
-    R.ndel[idx] = nd + 1;
+    R.rs[idx].ndel = nd + 1;
     if (nd == 0) {
         R.rec[idx].first_answer_delivery = now;
         R.rec[idx].first_answer_iter_start = iter_start;
@@ -627,8 +626,8 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
     unsigned m_c = 0;
     if (ln < len) {
         e_c = q[ln];
-        h_c = R.hot[e_c.x];
-        m_c = R.meta[e_c.x];
+        h_c = R.rs[e_c.x].h;
+        m_c = R.rs[e_c.x].meta;
     }
     if (32 + ln < len) e_n = q[32 + ln];
     for (int base = 0; base < len; base += 32) {
@@ -637,8 +636,8 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
         unsigned m_n = 0;
         uint2 e_nn = make_uint2(0, 0);
         if (k + 32 < len) {
-            h_n = R.hot[e_n.x];
-            m_n = R.meta[e_n.x];
+            h_n = R.rs[e_n.x].h;
+            m_n = R.rs[e_n.x].meta;
         }
         if (k + 64 < len) e_nn = q[k + 64];
         bool live = false, dem = false, cnd = false;
@@ -671,10 +670,10 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
                 unsigned seq = S.enq + 1 + rank;
                 h.z = (int)seq;
                 h.w = 0;
-                R.hot[e.x] = h;
-                R.qused[e.x] = 0;
+                R.rs[e.x].h = h;
+                R.rs[e.x].qused = 0;
                 m = m_set_qlow(m, true);
-                R.meta[e.x] = m;
+                R.rs[e.x].meta = m;
                 queue_ptr(R, i, 1)[lo_len + rank] = make_uint2(e.x, seq);
                 log_put(R, S.nlog + rank, S.now, kLDemote, i, (int)e.x, 0);
             }
@@ -694,7 +693,10 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
         // compact the queue in place (tombstones and demoted entries leave)
         unsigned km = __ballot_sync(FULL, keep);
         __syncwarp();
-        if (keep) q[w + __popc(km & lanemask_lt())] = e;
+        {
+            const int dst = w + __popc(km & lanemask_lt());
+            if (keep && dst != k) q[dst] = e;  // entries only move past tombstones
+        }
         w += __popc(km);
         // candidate record
         unsigned cm = __ballot_sync(FULL, cnd);
@@ -856,6 +858,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         const int cnt = min(32, n - base);
         int k = 0;
         while (k < cnt) {
+            S.adm_rounds++;
             const bool mine = valid && ln >= k;
             const bool evd = mine && ci_l >= A.b && my_rkv > 0;
             const bool bld = mine && !evd && fcfs_blocked && my_rkv == 0;
@@ -884,6 +887,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             if (__ballot_sync(FULL, fin && fc)) any_admitted = true;
             if (stop >= cnt) break;
             // ---- exact reference step for candidate `stop`
+            S.adm_slow++;
             const int ci = base + stop;
             const long long need = __shfl_sync(FULL, my_need, stop);
             const int cw = __shfl_sync(FULL, my_w, stop);
@@ -966,12 +970,12 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         int vi = 0;
         if (act) {
             vi = (int)R.elist[k];
-            int4 h = R.hot[vi];
+            int4 h = R.rs[vi].h;
             kv = h.x;
-            unsigned m = m_set_loc(R.meta[vi], LOC_CPU);
+            unsigned m = m_set_loc(R.rs[vi].meta, LOC_CPU);
             sd = swap_latency(R.prof, kv);
             if (sd > 0.0) m = m_set_swout(m, true);
-            R.meta[vi] = m;
+            R.rs[vi].meta = m;
             log_put(R, log0 + k, S.now, kLEvict, i, vi, 0);
         }
         long long tot = warp_sum_ll(kv);
@@ -1030,13 +1034,13 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
                  dnm = __ballot_sync(FULL, den), bm = __ballot_sync(FULL, inb);
         unsigned lt = lanemask_lt();
         if (sw) {
-            unsigned m = R.meta[c.x];
-            R.meta[c.x] = m_set_swin(m, true);
+            unsigned m = R.rs[c.x].meta;
+            R.rs[c.x].meta = m_set_swin(m, true);
             log_put(R, lsw + __popc(swm & lt), S.now, kLSwapIn, i, c.x, 0);
         }
         if (imm) {
-            unsigned m = R.meta[c.x];
-            R.meta[c.x] = m_set_loc(m, LOC_GPU);
+            unsigned m = R.rs[c.x].meta;
+            R.rs[c.x].meta = m_set_loc(m, LOC_GPU);
             log_put(R, limm + __popc(imm_m & lt), S.now, kLSwapIn, i, c.x, 0);
         }
         if (den) {
@@ -1092,7 +1096,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
 
 // --------------------------------------------------------------- events
 // engine.cpp:260-283
-DEVI void on_arrival(Rep& R, Scal& S, int idx) {
+DEVI int on_arrival(Rep& R, Scal& S, int idx) {
     if (lane_id() == 0) R.rec[idx].arrival = S.now;
     const bool pascal = R.policy == kPascal;
     if (pascal) compute_health(R, S);
@@ -1105,27 +1109,27 @@ DEVI void on_arrival(Rep& R, Scal& S, int idx) {
         m = m_set_loc(m, LOC_CPU);
         m = m_set_phase(m, sp.y > 0 ? PH_REASON : PH_ANSWER);
         if (lane_id() == 0) {
-            int4 h = R.hot[idx];
+            int4 h = R.rs[idx].h;
             h.x = sp.x;
-            R.hot[idx] = h;
-            R.meta[idx] = m;
+            R.rs[idx].h = h;
+            R.rs[idx].meta = m;
             R.rec[idx].prefill_complete = S.now;
             if (sp.y == 0) R.rec[idx].reasoning_end = S.now;
         }
         add_cpu(R, dst, sp.x);
         high = sp.y > 0 ? true : !pascal;
     } else {
-        if (lane_id() == 0) R.meta[idx] = m_set_phase(0u, PH_WAIT);
+        if (lane_id() == 0) R.rs[idx].meta = m_set_phase(0u, PH_WAIT);
         high = true;
     }
     __syncwarp();
     enqueue(R, S, dst, idx, high);
-    maybe_start(R, S, dst);
+    return dst;  // every handler ends with maybe_start on this instance
 }
 
 // engine.cpp:285-308
-DEVI void on_prefill_complete(Rep& R, Scal& S, int idx) {
-    unsigned m = R.meta[idx];
+DEVI int on_prefill_complete(Rep& R, Scal& S, int idx) {
+    unsigned m = R.rs[idx].meta;
     int i = m_owner(m);
     int4 sp = R.spec[idx];
     if (lane_id() == 0) R.s.busy[i] = 0;
@@ -1133,10 +1137,10 @@ DEVI void on_prefill_complete(Rep& R, Scal& S, int idx) {
     double iter_start = R.s.iter_start[i];
     __syncwarp();
     if (lane_id() == 0) {
-        int4 h = R.hot[idx];
+        int4 h = R.rs[idx].h;
         h.x = kv;
         if (sp.y == 0) h.y = 1;
-        R.hot[idx] = h;
+        R.rs[idx].h = h;
         R.rec[idx].prefill_complete = S.now;
     }
     __syncwarp();
@@ -1151,10 +1155,10 @@ DEVI void on_prefill_complete(Rep& R, Scal& S, int idx) {
         __syncwarp();
         if (1 == sp.z) {
             // phase = Answering; finish_request (engine.cpp:135-146)
-            int4 h = R.hot[idx];
+            int4 h = R.rs[idx].h;
             if (lane_id() == 0) {
                 dequeue_lane(R, idx, i, m, h.w);
-                R.meta[idx] = m_set_phase(m, PH_DONE);
+                R.rs[idx].meta = m_set_phase(m, PH_DONE);
                 R.rec[idx].completion = S.now;
             }
             // free_memory: waiting-prefill requests default to Gpu
@@ -1163,20 +1167,20 @@ DEVI void on_prefill_complete(Rep& R, Scal& S, int idx) {
             __syncwarp();
             emit(R, S, kLFinish, i, idx);
         } else {
-            if (lane_id() == 0) R.meta[idx] = m_set_phase(m, PH_ANSWER);
+            if (lane_id() == 0) R.rs[idx].meta = m_set_phase(m, PH_ANSWER);
             __syncwarp();
             emit(R, S, kLTransition, i, idx);
             if (R.policy == kPascal) pascal_transition(R, S, idx);
         }
     } else {
-        if (lane_id() == 0) R.meta[idx] = m_set_phase(m, PH_REASON);
+        if (lane_id() == 0) R.rs[idx].meta = m_set_phase(m, PH_REASON);
         __syncwarp();
     }
-    maybe_start(R, S, i);
+    return i;  // every handler ends with maybe_start on this instance
 }
 
 // engine.cpp:310-337: retire one decode iteration, batch members in plan order.
-DEVI void on_iteration_complete(Rep& R, Scal& S, int i) {
+DEVI int on_iteration_complete(Rep& R, Scal& S, int i) {
     if (lane_id() == 0) R.s.busy[i] = 0;
     int nb = R.s.blen[i];
     double iter_start = R.s.iter_start[i];
@@ -1196,10 +1200,10 @@ DEVI void on_iteration_complete(Rep& R, Scal& S, int i) {
     int qu_c = 0;
     if (ln < nb) {
         idx_c = (int)bin[ln];
-        h_c = R.hot[idx_c];
-        m_c = R.meta[idx_c];
+        h_c = R.rs[idx_c].h;
+        m_c = R.rs[idx_c].meta;
         sp_c = R.spec[idx_c];
-        qu_c = use_quanta ? R.qused[idx_c] : 0;
+        qu_c = use_quanta ? R.rs[idx_c].qused : 0;
     }
     if (32 + ln < nb) idx_n = (int)bin[32 + ln];
     for (int base = 0; base < nb; base += 32) {
@@ -1211,10 +1215,10 @@ DEVI void on_iteration_complete(Rep& R, Scal& S, int i) {
         int qu = qu_c;
         if (k + 32 < nb) {
             idx_c = idx_n;
-            h_c = R.hot[idx_n];
-            m_c = R.meta[idx_n];
+            h_c = R.rs[idx_n].h;
+            m_c = R.rs[idx_n].meta;
             sp_c = R.spec[idx_n];
-            qu_c = use_quanta ? R.qused[idx_n] : 0;
+            qu_c = use_quanta ? R.rs[idx_n].qused : 0;
         }
         if (k + 64 < nb) idx_n = (int)bin[k + 64];
         bool fresh_lost = false;
@@ -1276,9 +1280,9 @@ DEVI void on_iteration_complete(Rep& R, Scal& S, int i) {
                     log_put(R, S.nlog + lpos + 1, S.now, kLFinish, i, idx, 0);
                 }
                 if (fresh_lost) atomicSub(&R.s.afresh[i], 1);
-                R.hot[idx] = hw;
-                if (use_quanta) R.qused[idx] = qu;
-                if (mm != m) R.meta[idx] = mm;
+                R.rs[idx].h = hw;
+                if (use_quanta) R.rs[idx].qused = qu;
+                if (mm != m) R.rs[idx].meta = mm;
             }
             S.nlog += ltot;
             const unsigned fm = __ballot_sync(FULL, in && fin);
@@ -1291,10 +1295,10 @@ DEVI void on_iteration_complete(Rep& R, Scal& S, int i) {
             // ---- Pascal phase boundary for lane t, applied in batch order
             int tidx = __shfl_sync(FULL, idx, t);
             if (lane_id() == t) {
-                R.hot[idx] = h;
-                if (use_quanta) R.qused[idx] = qu;
+                R.rs[idx].h = h;
+                if (use_quanta) R.rs[idx].qused = qu;
                 if (fresh_lost) atomicSub(&R.s.afresh[i], 1);
-                R.meta[idx] = m_set_phase(m, PH_ANSWER);
+                R.rs[idx].meta = m_set_phase(m, PH_ANSWER);
                 R.rec[idx].reasoning_end = S.now;
             }
             __syncwarp();
@@ -1306,44 +1310,44 @@ DEVI void on_iteration_complete(Rep& R, Scal& S, int i) {
         }
     }
     __syncwarp();
-    maybe_start(R, S, i);
+    return i;  // every handler ends with maybe_start on this instance
 }
 
 // engine.cpp:339-349
-DEVI void on_swap_complete(Rep& R, Scal& S, int idx) {
-    unsigned m = R.meta[idx];
+DEVI int on_swap_complete(Rep& R, Scal& S, int idx) {
+    unsigned m = R.rs[idx].meta;
     int i = m_owner(m);
     if (lane_id() == 0) {
         unsigned mm = m;
         if (m_swout(m)) mm = m_set_swout(mm, false);
         else if (m_swin(m)) mm = m_set_loc(m_set_swin(mm, false), LOC_GPU);
-        R.meta[idx] = mm;
+        R.rs[idx].meta = mm;
     }
     __syncwarp();
     emit(R, S, kLSwapComplete, i, idx);
-    maybe_start(R, S, i);
+    return i;  // every handler ends with maybe_start on this instance
 }
 
 // engine.cpp:351-367
-DEVI void on_transfer_complete(Rep& R, Scal& S, int idx) {
-    unsigned m = R.meta[idx];
+DEVI int on_transfer_complete(Rep& R, Scal& S, int idx) {
+    unsigned m = R.rs[idx].meta;
     int dst = m_owner(m);
-    long long kv = R.hot[idx].x;
+    long long kv = R.rs[idx].h.x;
     bool fits = R.cap - R.s.gpu[dst] >= kv;
     if (fits) add_gpu(R, S, dst, kv);
     else add_cpu(R, dst, kv);
     if (lane_id() == 0) {
-        R.meta[idx] = m_set_loc(m, fits ? LOC_GPU : LOC_CPU);
-        R.qused[idx] = 0;
-        int4 h = R.hot[idx];
+        R.rs[idx].meta = m_set_loc(m, fits ? LOC_GPU : LOC_CPU);
+        R.rs[idx].qused = 0;
+        int4 h = R.rs[idx].h;
         h.w = 0;
-        R.hot[idx] = h;
+        R.rs[idx].h = h;
     }
     __syncwarp();
     enqueue(R, S, dst, idx, false);
     emit(R, S, kLTransferComplete, dst, idx);
     note_peak(S);
-    maybe_start(R, S, dst);
+    return dst;  // every handler ends with maybe_start on this instance
 }
 
 // ------------------------------------------------------------ the replica
@@ -1397,22 +1401,14 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     sp += smem_inst_bytes(max_ni);
     const bool resident = R.n <= n_smem;  // request state in shared memory
     if (resident) {
-        R.hot = reinterpret_cast<int4*>(sp);
-        R.spec = R.hot + n_smem;
+        R.rs = reinterpret_cast<ReqState*>(sp);
+        R.spec = reinterpret_cast<int4*>(R.rs + n_smem);
         R.blocked = reinterpret_cast<double*>(R.spec + n_smem);
-        R.meta = reinterpret_cast<unsigned*>(R.blocked + n_smem);
-        R.qused = reinterpret_cast<int*>(R.meta + n_smem);
-        R.ndel = R.qused + n_smem;
-        R.cursor = R.ndel + n_smem;
-        R.aoff = R.cursor + n_smem;
+        R.aoff = reinterpret_cast<int*>(R.blocked + n_smem);
     } else {
-        R.hot = a.hot + g;
+        R.rs = a.rs + g;
         R.spec = const_cast<int4*>(a.spec) + g;
         R.blocked = a.blocked + g;
-        R.meta = a.meta + g;
-        R.qused = a.qused + g;
-        R.ndel = a.ndel + g;
-        R.cursor = a.cursor + g;
         R.aoff = const_cast<int*>(a.aoff32) + g;
     }
     sp += smem_req_bytes(n_smem);
@@ -1436,11 +1432,13 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     }
     // reset per-request state (Simulator::run, engine.cpp:382-389)
     for (int k = lane_id(); k < R.n; k += 32) {
-        R.hot[k] = make_int4(0, 0, 0, 0);
-        R.meta[k] = m_set_phase(0u, PH_WAIT);
-        R.qused[k] = 0;
-        R.ndel[k] = 0;
-        R.cursor[k] = 0;
+        ReqState z0;
+        z0.h = make_int4(0, 0, 0, 0);
+        z0.meta = m_set_phase(0u, PH_WAIT);
+        z0.qused = 0;
+        z0.ndel = 0;
+        z0.cursor = 0;
+        R.rs[k] = z0;
         R.blocked[k] = 0.0;
         if (resident) {
             R.spec[k] = a.spec[g + k];
@@ -1469,6 +1467,7 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     S.peak = 0;
     S.nlog = 0;
     S.events = S.plans = S.visits = S.req_iters = S.ans_tokens = S.health = 0;
+    S.adm_rounds = S.adm_slow = 0;
     const long long heap_cap = (long long)R.n + R.ni + 1;
 
     while (S.status == 0) {
@@ -1500,20 +1499,23 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
             break;
         }
         S.now = dmax(S.now, et);
+        int plan_inst;
         switch (kind) {
-            case 0: on_arrival(R, S, (int)id); break;
-            case EV_PREFILL: on_prefill_complete(R, S, (int)id); break;
-            case EV_ITER: on_iteration_complete(R, S, (int)id); break;
-            case EV_SWAP: on_swap_complete(R, S, (int)id); break;
-            case EV_TRANSFER: on_transfer_complete(R, S, (int)id); break;
+            case 0: plan_inst = on_arrival(R, S, (int)id); break;
+            case EV_PREFILL: plan_inst = on_prefill_complete(R, S, (int)id); break;
+            case EV_ITER: plan_inst = on_iteration_complete(R, S, (int)id); break;
+            case EV_SWAP: plan_inst = on_swap_complete(R, S, (int)id); break;
+            default: plan_inst = on_transfer_complete(R, S, (int)id); break;
         }
+        // one inlined copy of the planner for all five handlers
+        maybe_start(R, S, plan_inst);
         if (S.hn + 1 > heap_cap && S.status == 0) S.status = kErrHeap;
     }
     if (S.status == 0 && S.done != R.n) S.status = kErrStall;
     // outputs the metric kernels read: delivered counts and blocked totals
     for (int k = lane_id(); k < R.n; k += 32) {
         R.rec[k].blocked = R.blocked[k];
-        if (resident) a.ndel[g + k] = R.ndel[k];
+        if (resident) a.rs[g + k].ndel = R.rs[k].ndel;
     }
     if (lane_id() == 0) {
         ReplicaOut o;
@@ -1527,6 +1529,8 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
         o.req_iters = S.req_iters;
         o.answer_tokens = S.ans_tokens;
         o.health_checks = S.health;
+        o.adm_rounds = S.adm_rounds;
+        o.adm_slow = S.adm_slow;
         o.now = S.now;
         a.out[r] = o;
     }

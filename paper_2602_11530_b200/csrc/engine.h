@@ -61,6 +61,7 @@ struct ReplicaOut {
     long long peak;  // peak sum of gpu_used (engine.cpp:75-79)
     long long nlog;  // log entries produced (may exceed log_cap)
     long long events, plans, visits, req_iters, answer_tokens, health_checks;
+    long long adm_rounds, adm_slow;
     double now;      // clock at the end of the run
 };
 
@@ -100,6 +101,17 @@ enum LogKind : int {
     kLTransferComplete
 };
 
+// Mutable per-request scheduling state, packed into one 32-byte sector so a
+// queue scan touches one sector per request (RequestState,
+// proj/include/pascalsim/instance.hpp:41-62).
+struct __align__(16) ReqState {
+    int4 h;           // {kv_tokens, tokens_generated, enqueue_seq (0 = not queued), quanta_exhausted}
+    unsigned meta;    // phase:2 | loc:2 | swin:1 | swout:1 | qlow:1 | owner:16 (<<8)
+    int qused;        // quantum_used_in_round
+    int ndel;         // delivered answer tokens
+    int cursor;       // digests known <= a past `now` (pacer health cursor)
+};
+
 // Batch-wide device arenas.
 struct Arena {
     const ReplicaDesc* desc;
@@ -112,11 +124,7 @@ struct Arena {
     const long long* aoff;  // absolute offset of the request's answer slots
     const int* aoff32;      // same, relative to the replica's first request
     // mutable request state
-    int4* hot;        // {kv, tokens, enqueue_seq (0 = not queued), quanta_exhausted}
-    unsigned* meta;   // phase:2 | loc:2 | swin:1 | swout:1 | qlow:1 | owner:16 (<<8)
-    int* qused;       // quantum_used_in_round
-    int* ndel;        // delivered answer tokens
-    int* cursor;      // digests known <= a past `now` (pacer health cursor)
+    ReqState* rs;     // per-request scheduling state (one 32-byte sector each)
     double* blocked;  // blocked_interval_total accumulator (global-resident replicas)
     RecOut* rec;
     double* dig;      // digest times (always)
@@ -150,6 +158,7 @@ struct DevSummary {
     double slo_rate, ttfat_attain, throughput;
     long long capacity, requests, req_iters, answer_tokens, events, plans, visits, health;
     long long slo_violations;
+    long long adm_rounds, adm_slow;
     int status, pad;
 };
 
@@ -176,7 +185,7 @@ struct RowArrays {
 // c_smem entries (37 B each). Larger replicas keep request state and heap in
 // HBM; plans with more queued requests than c_smem use the HBM scratch.
 PB_HD inline int smem_inst_bytes(int ni) { return ((ni * 64 + 16) + 15) / 16 * 16; }
-PB_HD inline int smem_req_bytes(int n_smem) { return (n_smem * 60 + 15) / 16 * 16; }
+PB_HD inline int smem_req_bytes(int n_smem) { return (n_smem * 60 + 15) / 16 * 16; }  // rs 32 + spec 16 + blocked 8 + aoff 4
 // Shared-memory event heap: sized for every pending event of a resident
 // replica; HBM-resident replicas start with h_slots slots (default 128) and
 // move their heap to HBM if it ever grows past them.

@@ -123,6 +123,7 @@ struct DeviceSummary {  // mirrors pascal_summary
     double slo_rate, ttfat_attain, throughput;
     long long capacity, requests, req_iters, answer_tokens, events, plans, visits, health;
     long long slo_violations;
+    long long adm_rounds, adm_slow;
     int status, pad;
 };
 

@@ -166,10 +166,11 @@ public:
     DevBuf<pb::ReplicaOut> d_out_, d_oout_;
     DevBuf<int> d_work_, d_omap_, d_rid_;
     DevBuf<double> d_arrival_, d_frac_;
-    DevBuf<int4> d_spec_, d_hot_, d_cand_, d_tmp_;
+    DevBuf<int4> d_spec_, d_cand_, d_tmp_;
+    DevBuf<pb::ReqState> d_rs_;
     DevBuf<long long> d_aoff_, d_biggest_, d_echo_, d_seg_;
-    DevBuf<unsigned> d_meta_, d_batch_, d_tmpq_, d_elist_, d_stack_;
-    DevBuf<int> d_qused_, d_ndel_, d_cursor_, d_aoff32_;
+    DevBuf<unsigned> d_batch_, d_tmpq_, d_elist_, d_stack_;
+    DevBuf<int> d_aoff32_;
     DevBuf<double> d_blocked_;
     DevBuf<pb::RecOut> d_rec_;
     DevBuf<double> d_dig_, d_del_;
@@ -319,11 +320,7 @@ void Batch::build() {
     d_spec_.ensure(rq);
     d_aoff_.ensure(rq);
     d_rid_.ensure(rq);
-    d_hot_.ensure(rq);
-    d_meta_.ensure(rq);
-    d_qused_.ensure(rq);
-    d_ndel_.ensure(rq);
-    d_cursor_.ensure(rq);
+    d_rs_.ensure(rq);
     d_aoff32_.ensure(rq);
     d_blocked_.ensure(rq);
     d_rec_.ensure(rq);
@@ -401,11 +398,7 @@ pb::Arena Batch::arena(bool oracle) const {
     a.aoff = d_aoff_.p;
     a.aoff32 = d_aoff32_.p;
     a.blocked = d_blocked_.p;
-    a.hot = d_hot_.p;
-    a.meta = d_meta_.p;
-    a.qused = d_qused_.p;
-    a.ndel = d_ndel_.p;
-    a.cursor = d_cursor_.p;
+    a.rs = d_rs_.p;
     a.rec = d_rec_.p;
     a.dig = d_dig_.p;
     a.del = d_del_.p;
@@ -534,10 +527,10 @@ void Batch::fetch_single(RunOutputs& o, bool records, bool log) {
         }
         o.aoff.resize(n);
         down(o.aoff.data(), d_aoff_.p, n * sizeof(long long));
-        std::vector<int> nd(n);
-        down(nd.data(), d_ndel_.p, n * sizeof(int));
-        // ndel travels in rec.pad for the dump writer
-        for (long long k = 0; k < n; ++k) o.rec[k].pad = nd[k];
+        std::vector<pb::ReqState> rs(n);
+        down(rs.data(), d_rs_.p, n * sizeof(pb::ReqState));
+        // the delivered count travels in rec.pad for the dump writer
+        for (long long k = 0; k < n; ++k) o.rec[k].pad = rs[k].ndel;
     }
     if (log) {
         pb::ReplicaOut ro;

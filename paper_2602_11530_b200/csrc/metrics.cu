@@ -37,7 +37,7 @@ __global__ void capacity_kernel(ReplicaDesc* desc, const ReplicaOut* oout, const
 
 __global__ void rows_kernel(const int* rid, const MetricParams* params, const int4* spec,
                             const long long* aoff, const RecOut* rec, const double* dig,
-                            const int* ndel, RowArrays rows, long long total) {
+                            const ReqState* rs, RowArrays rows, long long total) {
     long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= total) return;
     const MetricParams mp = params[rid[g]];
@@ -48,7 +48,7 @@ __global__ void rows_kernel(const int* rid, const MetricParams* params, const in
     double ttfat = __dsub_rn(r.first_answer_delivery, r.reasoning_end);
     // qoe (metrics.cpp:38-52)
     double q = 1.0;
-    int nd = ndel[g];
+    int nd = rs[g].ndel;
     long long n = sp.z;
     if (n >= 1 && nd > 0) {
         const double* d = dig + aoff[g];
@@ -113,6 +113,8 @@ __global__ void summary_kernel(const MetricParams* params, const ReplicaDesc* de
     s.visits = o.visits;
     s.health = o.health_checks;
     s.slo_violations = 0;
+    s.adm_rounds = o.adm_rounds;
+    s.adm_slow = o.adm_slow;
     s.status = o.status;
     s.pad = 0;
     if (o.status == 0 && n > 0) {
@@ -213,7 +215,7 @@ int launch_metrics(const Arena& a, const MetricParams* params, const long long* 
     }
     if (total > 0) {
         rows_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(
-            rid, params, a.spec, a.aoff, a.rec, a.dig, a.ndel, rows, total);
+            rid, params, a.spec, a.aoff, a.rec, a.dig, a.rs, rows, total);
         size_t bytes = *sort_tmp_bytes;
         if (cub::DeviceSegmentedSort::SortKeys(sort_tmp, bytes, rows.ttft, rows.ttft_sorted,
                                                (int)total, n_rep, seg, seg + 1,

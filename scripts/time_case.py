@@ -27,5 +27,6 @@ wall = time.perf_counter() - t0
 s = b.summaries()[0]
 tm = pb.last_timing()
 print(f"{name} reps={reps} T={t.request_iterations()} status={s.status} events={s.events} "
+      f"adm_rounds={s.admission_rounds} adm_slow={s.admission_slow_steps} "
       f"plans={s.plans} visits={s.candidate_visits} derive_ms={tm.derive_ms:.1f} "
       f"engine_ms={tm.engine_ms:.1f} wall_s={wall:.2f}")
