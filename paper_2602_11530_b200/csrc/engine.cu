@@ -138,6 +138,12 @@ DEVI double transfer_latency(const Profile& p, long long kv) {
     return __dadd_rn(p.fabric_latency, __ddiv_rn((double)kv, p.fabric_bandwidth));
 }
 DEVI double dmax(double a, double b) { return a < b ? b : a; }  // std::max(a, b)
+// swap_latency(p, kv) == 0.0 exactly when kv == 0 or the bandwidth is +inf:
+// for kv >= 1 and a finite positive bandwidth kv / bw >= 1 / DBL_MAX > 0.
+// (instance.cpp:259: zero-latency reloads join the batch immediately.)
+DEVI bool swap_is_instant(const Profile& p, long long kv) {
+    return kv == 0 || isinf(p.swap_bandwidth);
+}
 
 // ------------------------------------------------------- per-replica view
 struct Inst {  // shared-memory SoA for the replica's instances
@@ -737,11 +743,43 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
 
 // Stable partition of cand[s, e) by quanta ascending (== sort by (quanta,
 // enqueue_seq) since queues are in seq order). Nothing moves when all quanta
-// are equal, the common case.
+// are equal, the common case; a small quanta range is a two-pass counting
+// scatter (one ballot per bucket per chunk), a wide one falls back to one
+// selection pass per distinct value.
 DEVI void order_segment(const Rep& R, int s, int e, unsigned qmin, unsigned qmax, bool by_quanta) {
     if (!by_quanta || qmin >= qmax) return;
     for (int k = s + lane_id(); k < e; k += 32) R.tmp[k] = R.cand[k];
     __syncwarp();
+    const unsigned range = qmax - qmin + 1;
+    const unsigned lt = lanemask_lt();
+    if (range <= 32) {
+        int cnt = 0;  // lane b: size of bucket b
+        for (int base = s; base < e; base += 32) {
+            const int k = base + lane_id();
+            const unsigned b = k < e ? R.tmpq[k] - qmin : 0xffffffffu;
+            for (unsigned bb = 0; bb < range; ++bb) {
+                const unsigned m = __ballot_sync(FULL, b == bb);
+                if (lane_id() == (int)bb) cnt += __popc(m);
+            }
+        }
+        int total;
+        int off = s + warp_excl_scan(cnt, &total);  // lane b: first slot of bucket b
+        for (int base = s; base < e; base += 32) {
+            const int k = base + lane_id();
+            const bool valid = k < e;
+            const unsigned b = valid ? R.tmpq[k] - qmin : 0xffffffffu;
+            const int4 v = valid ? R.tmp[k] : make_int4(0, 0, 0, 0);
+            for (unsigned bb = 0; bb < range; ++bb) {
+                const unsigned m = __ballot_sync(FULL, b == bb);
+                if (!m) continue;
+                const int o = __shfl_sync(FULL, off, bb);
+                if (b == bb) R.cand[o + __popc(m & lt)] = v;
+                if (lane_id() == (int)bb) off += __popc(m);
+            }
+        }
+        __syncwarp();
+        return;
+    }
     int out = s;
     unsigned q = qmin;
     while (true) {
@@ -752,10 +790,11 @@ DEVI void order_segment(const Rep& R, int s, int e, unsigned qmin, unsigned qmax
             if (k < e) kq = R.tmpq[k];
             bool sel = kq == q;
             unsigned sm = __ballot_sync(FULL, sel);
-            if (sel) R.cand[out + __popc(sm & lanemask_lt())] = R.tmp[k];
+            if (sel) R.cand[out + __popc(sm & lt)] = R.tmp[k];
             out += __popc(sm);
-            next = min(next, warp_min_u(kq > q ? kq : 0xffffffffu));
+            next = min(next, kq > q ? kq : 0xffffffffu);  // lane-local
         }
+        next = warp_min_u(next);
         if (next == 0xffffffffu) break;
         q = next;
     }
@@ -869,20 +908,22 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
                 my_allow && (rb >= max(my_s, ci_l + 1) || (A.ns > 0 && stack_top >= my_s));
             const bool simple_sf = sf && my_rkv == 0 && !fcfs && any_admitted && !vict;
             const bool fc = act && !sf;
-            long long contrib = fc ? my_need : 0;
-            long long pin = contrib;
+            // needs are < 2^26 (host-validated KV limit), so a 32-bit prefix
+            // over 32 lanes cannot overflow
+            const int contrib = fc ? (int)my_need : 0;
+            int pin = contrib;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                long long y = __shfl_up_sync(FULL, pin, o);
+                int y = __shfl_up_sync(FULL, pin, o);
                 if (ln >= o) pin += y;
             }
-            const bool stop_here = (fc && pin > F) || (sf && !simple_sf);
+            const bool stop_here = (fc && (long long)pin > F) || (sf && !simple_sf);
             const unsigned sm = __ballot_sync(FULL, stop_here);
             const int stop = sm ? __ffs(sm) - 1 : cnt;
             const bool fin = mine && ln < stop;
             if (fin) st = fc ? CS_ADMIT : CS_DENY;
             // pin at lane stop-1 = admitted need so far (lanes < k contribute 0)
-            const long long taken = __shfl_sync(FULL, pin, max(stop - 1, 0));
+            const long long taken = __shfl_sync(FULL, pin, max(stop - 1, 0));  // widened
             if (stop > 0) A.free_ -= taken;
             if (__ballot_sync(FULL, fin && fc)) any_admitted = true;
             if (stop >= cnt) break;
@@ -930,7 +971,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         if (adm) {
             if (my_w & CF_WAIT) wt = true;
             else if (my_w & CF_RES) inb = true;
-            else if (swap_latency(R.prof, my.z) == 0.0) { imm = true; inb = true; }
+            else if (swap_is_instant(R.prof, my.z)) { imm = true; inb = true; }
             else sw = true;
         }
         const unsigned wm = __ballot_sync(FULL, wt);
@@ -1024,10 +1065,12 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         double sd = 0.0;
         if (adm && !(c.w & CF_WAIT)) {
             if (c.w & CF_RES) inb = true;
-            else {
+            else if (swap_is_instant(R.prof, c.z)) {
+                imm = true;
+                inb = true;
+            } else {
+                sw = true;
                 sd = swap_latency(R.prof, c.z);
-                if (sd == 0.0) { imm = true; inb = true; }
-                else sw = true;
             }
         }
         unsigned swm = __ballot_sync(FULL, sw), imm_m = __ballot_sync(FULL, imm),

@@ -109,8 +109,9 @@ void check_limits(const Job& j) {
         throw std::invalid_argument("trace exceeds the device engine limit (2^26-1 requests)");
     if (!(c.tpot > 0.0)) throw std::invalid_argument("target_tpot must be > 0");
     for (const Spec& s : *j.trace)
-        if (s.max_kv() > (long)INT_MAX / 2)
-            throw std::invalid_argument("request KV footprint exceeds the device engine limit");
+        if (s.max_kv() >= (1l << 26) - 1)
+            throw std::invalid_argument(
+                "request KV footprint exceeds the device engine limit (2^26 - 2 tokens)");
 }
 
 }  // namespace
