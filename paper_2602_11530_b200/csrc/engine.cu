@@ -1604,10 +1604,10 @@ int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slot
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // the unconstrained variant uses ~248 registers (8 warps per SM); more
-    // warps per SM -> the 128-register variant
-    const bool dense = (long long)blocks * warps_per_block > 8ll * sms;
-    auto kern = dense ? sched_kernel<4> : sched_kernel<1>;
+    // register budget by warps per SM: <= 8 -> unconstrained (~240 regs),
+    // <= 12 -> <= 168 regs, more -> <= 128 regs
+    const long long wpsm = ((long long)blocks * warps_per_block + sms - 1) / sms;
+    auto kern = wpsm <= 8 ? sched_kernel<1> : wpsm <= 12 ? sched_kernel<3> : sched_kernel<4>;
     if (smem > 48 * 1024) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
