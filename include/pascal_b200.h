@@ -81,6 +81,17 @@ pascal_status pascal_run_batch(const pascal_trace* const* traces,
 
 pascal_status pascal_last_timing(pascal_timing* out);
 
+/* The reference CLI's `pascalsim sweep` (proj/tools/pascalsim_cli.cpp:
+ * 299-342) as one device batch: every (policy, capacity fraction) point of
+ * the grid is simulated side by side, then <out_dir>/<policy>_f<%.2f>.{
+ * requests.csv,summary.txt,bins.csv} and <out_dir>/sweep.csv are written
+ * byte-identically to the sequential CLI loop. `base` supplies every other
+ * run-config field. */
+pascal_status pascal_sweep(const pascal_trace* t, const pascal_profile* p,
+                           const pascal_run_config* base, const char* const* policies,
+                           size_t n_policies, const double* fractions, size_t n_fractions,
+                           const char* out_dir);
+
 /* Parity: per-request records in the hex-float dump format of
  * oracle/ref_dump.cpp (id order) and, when event_log_path is non-NULL, the
  * pascal-events-v1 decision log. */

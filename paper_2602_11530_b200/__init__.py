@@ -16,5 +16,6 @@ from .api import (  # noqa: F401
     run_batch,
     run_config,
     run_dump,
+    run_sweep,
     set_device,
 )

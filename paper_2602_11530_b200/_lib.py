@@ -28,6 +28,7 @@ ABI_SYMBOLS = (
     "pascal_trace_load_hex", "pascal_trace_save_hex", "pascal_trace_from_arrays",
     "pascal_trace_get", "pascal_trace_request_iterations", "pascal_set_device",
     "pascal_device_available", "pascal_batch_set_groups", "pascal_batch_histograms",
+    "pascal_sweep",
 )
 HIST_BINS = 128
 
@@ -147,6 +148,8 @@ def bind(lib: C.CDLL, extensions: bool = True) -> C.CDLL:
         "pascal_device_available": (C.c_int, []),
         "pascal_batch_set_groups": (st, [P, C.POINTER(C.c_int), C.c_int]),
         "pascal_batch_histograms": (st, [P, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
+        "pascal_sweep": (st, [P, P, C.POINTER(RunConfig), C.POINTER(C.c_char_p), C.c_size_t,
+                              C.POINTER(C.c_double), C.c_size_t, C.c_char_p]),
     }
     for name, (res, args) in sig.items():
         if not extensions and not hasattr(lib, name):

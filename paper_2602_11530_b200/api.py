@@ -298,6 +298,16 @@ def run_batch(traces, profiles, cfgs) -> List[_lib.Summary]:
     return list(out)
 
 
+def run_sweep(trace: Trace, profile: Profile, base_cfg, policies: Sequence[str],
+          fractions: Sequence[float], out_dir: str) -> None:
+    """`pascalsim sweep` (proj/tools/pascalsim_cli.cpp:299-342) as one device
+    batch: per-point reports <out_dir>/<policy>_f<frac>.* and sweep.csv."""
+    pols = (C.c_char_p * len(policies))(*[_b(x) for x in policies])
+    fr = (C.c_double * len(fractions))(*fractions)
+    _check(_lib_().pascal_sweep(trace.handle, profile.handle, C.byref(base_cfg), pols,
+                                len(policies), fr, len(fractions), _b(out_dir)))
+
+
 def last_timing() -> _lib.Timing:
     t = _lib.Timing()
     _check(_lib_().pascal_last_timing(C.byref(t)))

@@ -7,6 +7,8 @@
 // are unguarded. pascal_run drives the sm_100a engine (engine_host.cpp).
 #include <algorithm>
 #include <cstdio>
+#include <filesystem>
+#include <memory>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -84,6 +86,40 @@ std::vector<size_t> id_order(const Trace& t) {
     std::iota(ord.begin(), ord.end(), size_t{0});
     std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return t[a].id < t[b].id; });
     return ord;
+}
+
+// metrics::build_report + the config echo of pascal_run (proj/src/capi.cpp:
+// 191-203): rows in id order, device-computed aggregates, tail bins.
+Report make_report(const Trace& t, const pascal_run_config& cfg, const RunCfg& rc,
+                   const std::vector<Row>& rows, const DeviceSummary& s, long long capacity) {
+    Report rep;
+    std::vector<std::pair<long, double>> pts;
+    for (size_t k : id_order(t)) {
+        rep.rows.push_back(rows[k]);
+        pts.emplace_back(rows[k].reasoning, rows[k].ttft);
+    }
+    if (!t.empty()) {
+        rep.ttft_mean = s.ttft_mean;
+        rep.ttft_p50 = s.ttft_p50;
+        rep.ttft_p90 = s.ttft_p90;
+        rep.ttft_p95 = s.ttft_p95;
+        rep.ttft_p99 = s.ttft_p99;
+        rep.slo_rate = s.slo_rate;
+        rep.ttfat_attain = s.ttfat_attain;
+        rep.throughput = s.throughput;
+        rep.bins = tail_bins(pts);
+    }
+    rep.echo = {
+        {"policy", cfg.policy},
+        {"instance_count", std::to_string(rc.instances)},
+        {"gpu_capacity", std::to_string(capacity)},
+        {"token_quantum", std::to_string(rc.quantum)},
+        {"demotion_threshold", std::to_string(rc.demotion)},
+        {"no_migration", std::to_string(cfg.no_migration != 0)},
+        {"non_adaptive", std::to_string(cfg.non_adaptive != 0)},
+        {"requests", std::to_string(t.size())},
+    };
+    return rep;
 }
 
 }  // namespace
@@ -226,35 +262,7 @@ pascal_status pascal_run(const pascal_trace* t, const pascal_profile* p,
         RunOutputs o = run_single(job, false, logf != nullptr);
         if (logf) write_event_log(logf, t->t, o.log);
 
-        Report rep;
-        std::vector<std::pair<long, double>> pts;
-        for (size_t k : id_order(t->t)) {
-            rep.rows.push_back(o.rows[k]);
-            pts.emplace_back(o.rows[k].reasoning, o.rows[k].ttft);
-        }
-        const DeviceSummary& s = o.summary;
-        if (!t->t.empty()) {
-            rep.ttft_mean = s.ttft_mean;
-            rep.ttft_p50 = s.ttft_p50;
-            rep.ttft_p90 = s.ttft_p90;
-            rep.ttft_p95 = s.ttft_p95;
-            rep.ttft_p99 = s.ttft_p99;
-            rep.slo_rate = s.slo_rate;
-            rep.ttfat_attain = s.ttfat_attain;
-            rep.throughput = s.throughput;
-            rep.bins = tail_bins(pts);
-        }
-        rep.echo = {
-            {"policy", cfg->policy},
-            {"instance_count", std::to_string(rc.instances)},
-            {"gpu_capacity", std::to_string(o.capacity)},
-            {"token_quantum", std::to_string(rc.quantum)},
-            {"demotion_threshold", std::to_string(rc.demotion)},
-            {"no_migration", std::to_string(cfg->no_migration != 0)},
-            {"non_adaptive", std::to_string(cfg->non_adaptive != 0)},
-            {"requests", std::to_string(t->t.size())},
-        };
-        write_report(rep, report_prefix);
+        write_report(make_report(t->t, *cfg, rc, o.rows, o.summary, o.capacity), report_prefix);
     });
 }
 
@@ -380,6 +388,64 @@ pascal_status pascal_run_batch(const pascal_trace* const* traces,
     pascal_batch_free(b);
     g_err = keep;
     return st;
+}
+
+pascal_status pascal_sweep(const pascal_trace* t, const pascal_profile* p,
+                           const pascal_run_config* base, const char* const* policies,
+                           size_t n_policies, const double* fractions, size_t n_fractions,
+                           const char* out_dir) {
+    return guarded([&] {
+        need(t && p && base && policies && fractions && out_dir, "null argument");
+        need(n_policies >= 1 && n_fractions >= 1, "sweep needs at least one point");
+        check_trace(t->t);
+        check_profile(p->p);
+        // grid points in the reference CLI's order (policy-major,
+        // proj/tools/pascalsim_cli.cpp:312-336), all simulated in one batch
+        std::vector<pascal_run_config> cfgs;
+        std::vector<Job> jobs;
+        for (size_t a = 0; a < n_policies; ++a) {
+            need(policies[a] != nullptr, "null argument");
+            for (size_t b = 0; b < n_fractions; ++b) {
+                pascal_run_config c = *base;
+                c.policy = policies[a];
+                c.capacity_fraction = fractions[b];
+                cfgs.push_back(c);
+            }
+        }
+        for (const pascal_run_config& c : cfgs) jobs.push_back(Job{&t->t, to_cfg(&c), p->p});
+        if (!device_available()) throw std::logic_error("no CUDA device available for the B200 engine");
+        std::unique_ptr<Batch, void (*)(Batch*)> b(batch_create(jobs), batch_free);
+        batch_execute(b.get());
+        std::vector<DeviceSummary> sum;
+        batch_summaries(b.get(), sum);
+        std::vector<std::vector<Row>> rows;
+        batch_rows(b.get(), rows);
+        std::error_code ignored;
+        std::filesystem::create_directories(out_dir, ignored);
+        std::string index =
+            "policy,capacity_fraction,slo_violation_rate,ttft_p50,ttft_p99,"
+            "ttfat_attainment,throughput\n";
+        for (size_t k = 0; k < cfgs.size(); ++k) {
+            if (sum[k].status != 0) throw std::logic_error(status_message(sum[k].status));
+            char tag[64];
+            std::snprintf(tag, sizeof tag, "%s_f%.2f", cfgs[k].policy, cfgs[k].capacity_fraction);
+            const std::string prefix = std::string(out_dir) + "/" + tag;
+            write_report(make_report(t->t, cfgs[k], jobs[k].cfg, rows[k], sum[k], sum[k].capacity),
+                         prefix);
+            // the CLI reads the values back from the written report
+            const Report rep = read_report(prefix);
+            char row[256];
+            std::snprintf(row, sizeof row, "%s,%.2f,%.6f,%.6f,%.6f,%.6f,%.6f\n", cfgs[k].policy,
+                          cfgs[k].capacity_fraction, rep.slo_rate, rep.ttft_p50, rep.ttft_p99,
+                          rep.ttfat_attain, rep.throughput);
+            index += row;
+        }
+        const std::string idx = std::string(out_dir) + "/sweep.csv";
+        FILE* f = std::fopen(idx.c_str(), "w");
+        if (!f) throw std::runtime_error("cannot open: " + idx);
+        std::fwrite(index.data(), 1, index.size(), f);
+        std::fclose(f);
+    });
 }
 
 pascal_status pascal_last_timing(pascal_timing* out) {

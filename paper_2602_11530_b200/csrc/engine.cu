@@ -106,20 +106,6 @@ DEVI int warp_excl_scan(int v, int* total) {
     *total = __shfl_sync(FULL, x, 31);
     return x - v;
 }
-// Lowest key, ties to the lowest id (argmin_by's strict '<' in id order,
-// proj/src/cluster.cpp:10-23).
-DEVI void warp_argmin(long long& key, int& id) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        long long k2 = __shfl_xor_sync(FULL, key, o);
-        int i2 = __shfl_xor_sync(FULL, id, o);
-        if (k2 < key || (k2 == key && i2 < id)) {
-            key = k2;
-            id = i2;
-        }
-    }
-}
-
 // -------------------------------------------------------------- costmodel
 // proj/src/costmodel.cpp:35-51, operation order preserved (device code is
 // compiled with -fmad=false so no contraction happens).
@@ -174,8 +160,11 @@ struct Rep {
     ReqState* rs;
     double* blocked;
     RecOut* rec;
-    double* dig;  // this replica's digest arena
-    double* del;  // this replica's delivery arena
+    PacerHot* ph;
+    double* bpv;  // this replica's breakpoint arenas (indexed by aoff)
+    int* bpk;
+    double* dig;  // this replica's full digest arena (kRecordDeliv)
+    double* del;  // this replica's delivery arena (kRecordDeliv)
     uint2* qent;
     long long qcap;
     unsigned* batch;
@@ -219,16 +208,21 @@ DEVI uint2* queue_ptr(const Rep& R, int i, int low) {
 }
 
 // ------------------------------------------------------------- event log
+// Cold paths live out of line (__noinline__): the kernel's hot loop must stay
+// small for the instruction cache (L1.5 I$ is 32 KB per SM; the fully inlined
+// kernel was 180 KB and stalled on instruction fetch ~30% of the time).
+__device__ __noinline__ void log_store(LogEnt* log, long long pos, double t, int kind, int inst,
+                                       int req, int det) {
+    LogEnt e;
+    e.t = t;
+    e.req = req;
+    e.inst = inst;
+    e.kind = kind;
+    e.detail = det;
+    log[pos] = e;
+}
 DEVI void log_put(const Rep& R, long long pos, double t, int kind, int inst, int req, int det) {
-    if ((R.flags & kLogEvents) && pos < R.logcap) {
-        LogEnt e;
-        e.t = t;
-        e.req = req;
-        e.inst = inst;
-        e.kind = kind;
-        e.detail = det;
-        R.log[pos] = e;
-    }
+    if ((R.flags & kLogEvents) && pos < R.logcap) log_store(R.log, pos, t, kind, inst, req, det);
 }
 // Scalar emit (engine.cpp:91-97): one line at the end of the log.
 DEVI void emit(const Rep& R, Scal& S, int kind, int inst, int req, int det = 0) {
@@ -242,6 +236,21 @@ DEVI void emit(const Rep& R, Scal& S, int kind, int inst, int req, int det = 0) 
 DEVI bool ev_less(double ta, unsigned long long ka, double tb, unsigned long long kb) {
     return ta < tb || (ta == tb && ka < kb);
 }
+__device__ __noinline__ void heap_spill(HeapEnt* dst, const HeapEnt* src, int hn) {
+    for (int k = 1 + lane_id(); k <= hn; k += 32) dst[k] = src[k];
+    __syncwarp();
+}
+__device__ __noinline__ void heap_sift_up(HeapEnt* h, int pos, double t, unsigned long long key) {
+    while (pos > 1) {
+        int p = pos >> 1;
+        HeapEnt pe = h[p];
+        if (!ev_less(t, key, pe.t, pe.key)) break;
+        h[pos] = pe;
+        pos = p;
+    }
+    h[pos].t = t;
+    h[pos].key = key;
+}
 DEVI void heap_push(const Rep& R, Scal& S, double t, unsigned kind, unsigned id) {
     // engine.cpp:85-89
     if (t < S.now - 1e-12) {
@@ -252,24 +261,12 @@ DEVI void heap_push(const Rep& R, Scal& S, double t, unsigned kind, unsigned id)
     if (S.hn + 1 >= S.heap_slots && S.heap != R.heap) {
         // shared-memory heap full: move it to the HBM heap (sized for every
         // pending event) and stay there
-        for (int k = 1 + lane_id(); k <= S.hn; k += 32) R.heap[k] = S.heap[k];
-        __syncwarp();
+        heap_spill(R.heap, S.heap, S.hn);
         S.heap = R.heap;
         S.heap_slots = (long long)R.n + R.ni + 2;
     }
     int pos = ++S.hn;
-    if (lane_id() == 0) {
-        HeapEnt* h = S.heap;
-        while (pos > 1) {
-            int p = pos >> 1;
-            HeapEnt pe = h[p];
-            if (!ev_less(t, key, pe.t, pe.key)) break;
-            h[pos] = pe;
-            pos = p;
-        }
-        h[pos].t = t;
-        h[pos].key = key;
-    }
+    if (lane_id() == 0) heap_sift_up(S.heap, pos, t, key);
     __syncwarp();
 }
 DEVI HeapEnt heap_pop(const Rep& R, Scal& S) {
@@ -310,9 +307,7 @@ DEVI HeapEnt heap_pop(const Rep& R, Scal& S) {
 // entry is live iff hot[idx].seq == seq (dequeue zeroes the request's seq).
 // Live entries keep ascending-seq order, i.e. the order of the reference's
 // std::vector queues (engine.cpp:111-126).
-DEVI void queue_compact(const Rep& R, int i, int low) {
-    uint2* q = queue_ptr(R, i, low);
-    int len = low ? R.s.lo_len[i] : R.s.hi_len[i];
+__device__ __noinline__ int queue_compact_impl(uint2* q, int len, const ReqState* rs) {
     int w = 0;
     for (int base = 0; base < len; base += 32) {
         int k = base + lane_id();
@@ -320,7 +315,7 @@ DEVI void queue_compact(const Rep& R, int i, int low) {
         uint2 e = make_uint2(0, 0);
         if (k < len) {
             e = q[k];
-            live = (unsigned)R.rs[e.x].h.z == e.y;
+            live = (unsigned)rs[e.x].h.z == e.y;
         }
         unsigned mk = __ballot_sync(FULL, live);
         __syncwarp();
@@ -331,6 +326,11 @@ DEVI void queue_compact(const Rep& R, int i, int low) {
         w += __popc(mk);
     }
     __syncwarp();
+    return w;
+}
+DEVI void queue_compact(const Rep& R, int i, int low) {
+    const int len = low ? R.s.lo_len[i] : R.s.hi_len[i];
+    const int w = queue_compact_impl(queue_ptr(R, i, low), len, R.rs);
     if (lane_id() == 0) {
         if (low) R.s.lo_len[i] = w;
         else R.s.hi_len[i] = w;
@@ -380,28 +380,64 @@ DEVI void dequeue_lane(const Rep& R, int idx, int owner, unsigned m, int quanta)
 }
 
 // ------------------------------------------------------ monitor snapshots
+// What the snapshot scan reads; passed by value to the out-of-line scan so
+// the replica's register-resident state never has its address taken.
+struct HealthView {
+    const uint2* qent;
+    long long qcap;
+    const int* lo_len;
+    int* healthy;
+    ReqState* rs;
+    const int4* spec;
+    PacerHot* ph;
+    const int* bpk;
+    const double* bpv;
+    const int* aoff;
+    double tpot;
+    long long slack;
+    int ni;
+};
+
 // PacerState::healthy (instance.cpp:22-33) with a monotone cursor: `now`
-// never decreases, so the count of digests <= now only grows.
-DEVI bool pacer_healthy(const Rep& R, Scal& S, int idx, int answering) {
-    int nd = R.rs[idx].ndel;
+// never decreases and digests only grow, so the count of digests <= now only
+// grows. Digests are regenerated from the breakpoints (engine.h PacerHot):
+// d_c is the next breakpoint's value when its token index is c, else
+// d_{c-1} + tpot — the reference's own addition.
+DEVI bool pacer_healthy(const HealthView& V, double now, int idx, int answering) {
+    int nd = V.rs[idx].ndel;
     if (nd == 0) return true;
-    const double* d = R.dig + R.aoff[idx];
-    double t0 = d[0];
-    long long expected = 1 + (long long)floor(__ddiv_rn(__dsub_rn(S.now, t0), R.tpot));
+    PacerHot p = V.ph[idx];
+    long long expected = 1 + (long long)floor(__ddiv_rn(__dsub_rn(now, p.t0), V.tpot));
     if (expected > answering) expected = answering;
-    int c = R.rs[idx].cursor;
-    while (c < nd && d[c] <= S.now) ++c;
-    R.rs[idx].cursor = c;
-    return (long long)c >= expected - R.slack;
+    int c = V.rs[idx].cursor;
+    if (c < nd) {
+        const int off = V.aoff[idx];
+        const int c0 = c;
+        while (c < nd) {
+            const bool isbp = p.jn < p.nbp && V.bpk[off + p.jn] == c;
+            const double v = isbp ? V.bpv[off + p.jn] : __dadd_rn(p.dcur, V.tpot);
+            if (!(v <= now)) break;
+            p.dcur = v;
+            ++c;
+            if (isbp) ++p.jn;
+        }
+        if (c != c0) {
+            V.rs[idx].cursor = c;
+            V.ph[idx].dcur = p.dcur;
+            V.ph[idx].jn = p.jn;
+        }
+    }
+    return (long long)c >= expected - V.slack;
 }
 
 // t_i for every instance (instance.cpp:67-74): AND over low-queue Answering
-// members. Results go to R.s.healthy[].
-DEVI void compute_health(const Rep& R, Scal& S) {
+// members, into healthy[]. Returns the number of pacer evaluations. One
+// out-of-line copy serves arrivals and both phase-boundary sites.
+__device__ __noinline__ long long health_scan(const HealthView V, double now) {
     long long checks = 0;
-    for (int i = 0; i < R.ni; ++i) {
-        uint2* q = queue_ptr(R, i, 1);
-        int len = R.s.lo_len[i];
+    for (int i = 0; i < V.ni; ++i) {
+        const uint2* q = V.qent + (long long)(2 * i + 1) * V.qcap;
+        int len = V.lo_len[i];
         bool ok = true;
         for (int base = 0; base < len && ok; base += 32) {
             int k = base + lane_id();
@@ -409,71 +445,83 @@ DEVI void compute_health(const Rep& R, Scal& S) {
             bool chk = false;
             if (k < len) {
                 uint2 e = q[k];
-                int4 h = R.rs[e.x].h;
+                int4 h = V.rs[e.x].h;
                 if ((unsigned)h.z == e.y) {
-                    unsigned m = R.rs[e.x].meta;
+                    unsigned m = V.rs[e.x].meta;
                     if (m_phase(m) == PH_ANSWER) {
                         chk = true;
-                        bad = !pacer_healthy(R, S, (int)e.x, R.spec[e.x].z);
+                        bad = !pacer_healthy(V, now, (int)e.x, V.spec[e.x].z);
                     }
                 }
             }
             checks += __popc(__ballot_sync(FULL, chk));
             ok = __ballot_sync(FULL, bad) == 0;
         }
-        if (lane_id() == 0) R.s.healthy[i] = ok ? 1 : 0;
+        if (lane_id() == 0) V.healthy[i] = ok ? 1 : 0;
     }
-    S.health += checks;
     __syncwarp();
+    return checks;
 }
 
-// Alg. 1 / baseline routing (cluster.cpp:27-33,59-62): argmin m_i, healthy
-// instances first when `health` is set.
+DEVI void compute_health(const Rep& R, Scal& S) {
+    HealthView V;
+    V.qent = R.qent;
+    V.qcap = R.qcap;
+    V.lo_len = R.s.lo_len;
+    V.healthy = R.s.healthy;
+    V.rs = R.rs;
+    V.spec = R.spec;
+    V.ph = R.ph;
+    V.bpk = R.bpk;
+    V.bpv = R.bpv;
+    V.aoff = R.aoff;
+    V.tpot = R.tpot;
+    V.slack = R.slack;
+    V.ni = R.ni;
+    S.health += health_scan(V, S.now);
+}
+
+// Instance selection (cluster.cpp:10-44,59-62), lowest key with ties to the
+// lowest id (argmin_by's strict '<' in id order). Keys are non-negative and
+// below 2^54 (token sums of < 2^26 requests of < 2^26 tokens), ids below 512,
+// so (key, id) packs into one u64 and a plain warp min is the argmin.
+//   SEL_M:         argmin m_i = gpu + cpu (baseline routing)
+//   SEL_M_HEALTHY: argmin m_i over healthy instances, else over all (Alg. 1)
+//   SEL_ANSWER:    argmin r_i over healthy, else argmin r_i + a_i (Alg. 2)
+enum : int { SEL_M = 0, SEL_M_HEALTHY = 1, SEL_ANSWER = 2 };
+__device__ __noinline__ int select_instance(int ni, int mode, const long long* gpu,
+                                            const long long* cpu, const int* hcount,
+                                            const int* afresh, const int* healthy) {
+    const unsigned long long NONE = ~0ull;
+    unsigned long long best = NONE;
+    for (int pass = (mode == SEL_M ? 1 : 0); pass < 2 && best == NONE; ++pass) {
+        for (int base = 0; base < ni; base += 32) {
+            const int i = base + lane_id();
+            unsigned long long v = NONE;
+            if (i < ni && (pass == 1 || healthy[i])) {
+                const long long k = mode == SEL_ANSWER
+                                        ? (pass == 0 ? (long long)hcount[i]
+                                                     : (long long)hcount[i] + afresh[i])
+                                        : gpu[i] + cpu[i];
+                v = ((unsigned long long)k << 9) | (unsigned)i;
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long y = __shfl_xor_sync(FULL, v, o);
+                v = y < v ? y : v;
+            }
+            best = v < best ? v : best;
+        }
+    }
+    return (int)(best & 511u);
+}
 DEVI int select_by_m(const Rep& R, bool health) {
-    long long bk = LLONG_MAX;
-    int bid = INT_MAX;
-    for (int pass = 0; pass < (health ? 2 : 1) && bid == INT_MAX; ++pass) {
-        bool only_healthy = health && pass == 0;
-        for (int base = 0; base < R.ni; base += 32) {
-            int i = base + lane_id();
-            long long k = LLONG_MAX;
-            int id = INT_MAX;
-            if (i < R.ni && (!only_healthy || R.s.healthy[i])) {
-                k = R.s.gpu[i] + R.s.cpu[i];
-                id = i;
-            }
-            warp_argmin(k, id);
-            if (k < bk || (k == bk && id < bid)) {
-                bk = k;
-                bid = id;
-            }
-        }
-    }
-    return bid;
+    return select_instance(R.ni, health ? SEL_M_HEALTHY : SEL_M, R.s.gpu, R.s.cpu, R.s.hcount,
+                           R.s.afresh, R.s.healthy);
 }
-
-// Alg. 2 (cluster.cpp:35-44): healthy argmin r_i, else argmin r_i + a_i.
 DEVI int select_answering(const Rep& R) {
-    long long bk = LLONG_MAX;
-    int bid = INT_MAX;
-    for (int pass = 0; pass < 2 && bid == INT_MAX; ++pass) {
-        for (int base = 0; base < R.ni; base += 32) {
-            int i = base + lane_id();
-            long long k = LLONG_MAX;
-            int id = INT_MAX;
-            if (i < R.ni && (pass == 1 || R.s.healthy[i])) {
-                k = pass == 0 ? (long long)R.s.hcount[i]
-                              : (long long)R.s.hcount[i] + (long long)R.s.afresh[i];
-                id = i;
-            }
-            warp_argmin(k, id);
-            if (k < bk || (k == bk && id < bid)) {
-                bk = k;
-                bid = id;
-            }
-        }
-    }
-    return bid;
+    return select_instance(R.ni, SEL_ANSWER, R.s.gpu, R.s.cpu, R.s.hcount, R.s.afresh,
+                           R.s.healthy);
 }
 
 // ------------------------------------------------------------- handlers
@@ -541,15 +589,35 @@ DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
     emit(R, S, kLMigrate, cur, idx, target);
 }
 
-// Shared by the R == 0 path of prefill completion: a single answer delivery
-// (PacerState::on_delivery, instance.cpp:10-20 + engine.cpp:148-156).
+// One answer delivery (PacerState::on_delivery, instance.cpp:10-20 +
+// engine.cpp:148-156); shared by the R == 0 path of prefill completion.
+// Records a breakpoint when the digest is the generation time itself.
 DEVI void deliver_lane(const Rep& R, double now, int idx, double iter_start) {
     int nd = R.rs[idx].ndel;
     const int off = R.aoff[idx];
-    double* d = R.dig + off;
-    double v = nd == 0 ? now : dmax(now, __dadd_rn(d[nd - 1], R.tpot));
-    d[nd] = v;
-    if (R.flags & kRecordDeliv) R.del[off + nd] = now;
+    PacerHot* pp = R.ph + idx;
+    double v;
+    bool bp;
+    if (nd == 0) {
+        v = now;
+        bp = true;
+        pp->t0 = now;
+    } else {
+        const double x = __dadd_rn(pp->dlast, R.tpot);
+        bp = !(now < x);  // std::max(gen, prev + tpot) picks gen
+        v = bp ? now : x;
+    }
+    if (bp) {
+        const int j = pp->nbp;
+        R.bpv[off + j] = now;
+        R.bpk[off + j] = nd;
+        pp->nbp = j + 1;
+    }
+    pp->dlast = v;
+    if (R.flags & kRecordDeliv) {
+        R.dig[off + nd] = v;
+        R.del[off + nd] = now;
+    }
     R.rs[idx].ndel = nd + 1;
     if (nd == 0) {
         R.rec[idx].first_answer_delivery = now;
@@ -613,11 +681,14 @@ DEVI void pop_stack(const Rep& R, Adm& A, int s, long long need) {
 
 // Gather one queue (demoting first when Pascal scans the high queue) into
 // cand[nt..] in queue order; quanta go to tmpq for the partition. Returns the
-// min / max quanta of the gathered candidates and how many have quanta 0.
+// min / max quanta of the gathered candidates, how many have quanta 0, the
+// highest position holding a resident KV footprint (-1 if none) and, when
+// `count_q`, the quanta histogram for the partition (lane b: quanta == b).
 DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned& qmin,
-                       unsigned& qmax, int& zero_q) {
+                       unsigned& qmax, int& zero_q, int& rbpos, bool count_q, int& qcnt) {
     unsigned lmin = 0xffffffffu, lmax = 0;
     int lzero = 0;
+    int lrb = -1;
     uint2* q = queue_ptr(R, i, low);
     int len = low ? R.s.lo_len[i] : R.s.hi_len[i];
     const bool demote = (R.policy == kPascal) && !low;
@@ -727,12 +798,23 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
             lmin = min(lmin, (unsigned)h.w);
             lmax = max(lmax, (unsigned)h.w);
             lzero += h.w == 0;
+            if ((flags & CF_RES) && h.x > 0) lrb = pos;  // positions grow per lane
+        }
+        if (count_q) {  // one ballot per distinct quanta value in the chunk
+            unsigned todo = cm;
+            while (todo) {
+                const unsigned v = __shfl_sync(FULL, (unsigned)h.w, __ffs(todo) - 1);
+                const unsigned m = __ballot_sync(FULL, cnd && (unsigned)h.w == v);
+                if (ln == (int)v) qcnt += __popc(m);
+                todo &= ~m;
+            }
         }
         nt += __popc(cm);
     }
     qmin = warp_min_u(lmin);
     qmax = warp_max_u(lmax);
     zero_q = warp_sum(lzero);
+    rbpos = (int)warp_max_u((unsigned)(lrb + 1)) - 1;
     __syncwarp();
     if (lane_id() == 0) {
         if (low) R.s.lo_len[i] = w;
@@ -741,56 +823,64 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
     __syncwarp();
 }
 
-// Stable partition of cand[s, e) by quanta ascending (== sort by (quanta,
-// enqueue_seq) since queues are in seq order). Nothing moves when all quanta
-// are equal, the common case; a small quanta range is a two-pass counting
-// scatter (one ballot per bucket per chunk), a wide one falls back to one
-// selection pass per distinct value.
-DEVI void order_segment(const Rep& R, int s, int e, unsigned qmin, unsigned qmax, bool by_quanta) {
-    if (!by_quanta || qmin >= qmax) return;
-    for (int k = s + lane_id(); k < e; k += 32) R.tmp[k] = R.cand[k];
-    __syncwarp();
-    const unsigned range = qmax - qmin + 1;
+// Stable partition of src[s, e) into dst[s, e) by quanta ascending (== sort
+// by (quanta, enqueue_seq) since queues are in seq order). `part` false: plain
+// copy. Quanta below 32 (the common case): one scatter pass, bucket offsets
+// from the histogram gather_queue built (lane b: bucket b), one ballot per
+// distinct quanta value per chunk; wider ranges: one selection pass per
+// distinct value. Returns the highest dst position holding a resident KV
+// footprint (-1 if none) when `part`, else `rb_in`.
+DEVI int order_segment(const Rep& R, const int4* src, int4* dst, int s, int e, unsigned qmin,
+                       unsigned qmax, bool part, int qcnt, int rb_in) {
+    const int ln = lane_id();
+    if (!part) {
+        if (src != dst)
+            for (int k = s + ln; k < e; k += 32) dst[k] = src[k];
+        return rb_in;
+    }
     const unsigned lt = lanemask_lt();
-    if (range <= 32) {
-        int cnt = 0;  // lane b: size of bucket b
-        for (int base = s; base < e; base += 32) {
-            const int k = base + lane_id();
-            const unsigned b = k < e ? R.tmpq[k] - qmin : 0xffffffffu;
-            for (unsigned bb = 0; bb < range; ++bb) {
-                const unsigned m = __ballot_sync(FULL, b == bb);
-                if (lane_id() == (int)bb) cnt += __popc(m);
-            }
-        }
+    int lrb = -1;
+    if (qmax < 32) {
         int total;
-        int off = s + warp_excl_scan(cnt, &total);  // lane b: first slot of bucket b
+        int off = s + warp_excl_scan(qcnt, &total);  // lane b: first slot of bucket b
         for (int base = s; base < e; base += 32) {
-            const int k = base + lane_id();
+            const int k = base + ln;
             const bool valid = k < e;
-            const unsigned b = valid ? R.tmpq[k] - qmin : 0xffffffffu;
-            const int4 v = valid ? R.tmp[k] : make_int4(0, 0, 0, 0);
-            for (unsigned bb = 0; bb < range; ++bb) {
-                const unsigned m = __ballot_sync(FULL, b == bb);
-                if (!m) continue;
-                const int o = __shfl_sync(FULL, off, bb);
-                if (b == bb) R.cand[o + __popc(m & lt)] = v;
-                if (lane_id() == (int)bb) off += __popc(m);
+            const unsigned q = valid ? R.tmpq[k] : 0xffffffffu;
+            const int4 v = valid ? src[k] : make_int4(0, 0, 0, 0);
+            unsigned todo = __ballot_sync(FULL, valid);
+            while (todo) {
+                const unsigned qv = __shfl_sync(FULL, q, __ffs(todo) - 1);
+                const unsigned m = __ballot_sync(FULL, q == qv);
+                const int o = __shfl_sync(FULL, off, qv);
+                if (q == qv) {
+                    const int d = o + __popc(m & lt);
+                    dst[d] = v;
+                    if (cand_rkv(v) > 0) lrb = max(lrb, d);
+                }
+                if (ln == (int)qv) off += __popc(m);
+                todo &= ~m;
             }
         }
         __syncwarp();
-        return;
+        return (int)warp_max_u((unsigned)(lrb + 1)) - 1;
     }
     int out = s;
     unsigned q = qmin;
     while (true) {
         unsigned next = 0xffffffffu;
         for (int base = s; base < e; base += 32) {
-            int k = base + lane_id();
+            int k = base + ln;
             unsigned kq = 0xffffffffu;
             if (k < e) kq = R.tmpq[k];
             bool sel = kq == q;
             unsigned sm = __ballot_sync(FULL, sel);
-            if (sel) R.cand[out + __popc(sm & lt)] = R.tmp[k];
+            if (sel) {
+                const int d = out + __popc(sm & lt);
+                const int4 v = src[k];
+                dst[d] = v;
+                if (cand_rkv(v) > 0) lrb = max(lrb, d);
+            }
             out += __popc(sm);
             next = min(next, kq > q ? kq : 0xffffffffu);  // lane-local
         }
@@ -799,6 +889,7 @@ DEVI void order_segment(const Rep& R, int s, int e, unsigned qmin, unsigned qmax
         q = next;
     }
     __syncwarp();
+    return (int)warp_max_u((unsigned)(lrb + 1)) - 1;
 }
 
 // Highest candidate index j < b with a resident KV footprint (a potential
@@ -836,19 +927,45 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     const bool classed = pascal;
 
     // ---- gather (+ demotion) and priority order (instance.cpp:113-141)
-    int nt = 0, z0 = 0, z1 = 0;
+    const bool by_quanta = R.policy == kRr || pascal;
+    // segment 0 = high queue, segment 1 = low queue (Pascal class 1); one
+    // code copy for both (instruction-cache footprint)
+    int nt = 0, z0 = 0, rb0 = -1, rb1 = -1, qc0 = 0, qc1 = 0, c1 = 0;
     unsigned qmin0 = 0xffffffffu, qmax0 = 0, qmin1 = 0xffffffffu, qmax1 = 0;
-    gather_queue(R, S, i, 0, nt, qmin0, qmax0, z0);
-    int c1 = nt;
-    if (pascal) gather_queue(R, S, i, 1, nt, qmin1, qmax1, z1);
+    const int segs = pascal ? 2 : 1;
+#pragma unroll 1
+    for (int sg = 0; sg < segs; ++sg) {
+        unsigned qmn, qmx;
+        int zq, rbs, qc = 0;
+        c1 = nt;
+        gather_queue(R, S, i, sg, nt, qmn, qmx, zq, rbs, by_quanta, qc);
+        if (sg == 0) {
+            qmin0 = qmn, qmax0 = qmx, z0 = zq, rb0 = rbs, qc0 = qc;
+        } else {
+            qmin1 = qmn, qmax1 = qmx, rb1 = rbs, qc1 = qc;
+        }
+    }
+    if (!pascal) c1 = nt;
     const int n = nt;
     S.visits += n;
-    const bool by_quanta = R.policy == kRr || pascal;
-    if (pascal) {
-        order_segment(R, 0, c1, qmin0, qmax0, true);
-        order_segment(R, c1, n, qmin1, qmax1, true);
-    } else {
-        order_segment(R, 0, n, qmin0, qmax0, by_quanta);
+    // priority order: the queue-ordered segments are partitioned into the
+    // second scratch buffer, which then becomes the candidate array
+    const bool part0 = by_quanta && qmin0 < qmax0;
+    const bool part1 = pascal && qmin1 < qmax1;
+    if (part0 || part1) {
+        int4* src = R.cand;
+        int4* dst = R.tmp;
+#pragma unroll 1
+        for (int sg = 0; sg < segs; ++sg) {
+            const bool one = sg == 1;
+            const int r = order_segment(R, src, dst, one ? c1 : 0, one ? n : c1,
+                                        one ? qmin1 : qmin0, one ? qmax1 : qmax0,
+                                        one ? part1 : part0, one ? qc1 : qc0, one ? rb1 : rb0);
+            if (one) rb1 = r;
+            else rb0 = r;
+        }
+        R.cand = dst;
+        R.tmp = src;
     }
     // k0: first class-0 candidate with quanta > 0 (victims of a class-0
     // admission form the suffix [k0, n), instance.cpp:158-162); after the
@@ -873,7 +990,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     A.ns = 0;
     A.ne = 0;
     int stack_top = -1;
-    int rb = find_rb(R, n);
+    int rb = rb1 >= 0 ? rb1 : rb0;
     bool any_admitted = false, fcfs_blocked = false;
     const bool fcfs = R.policy == kFcfs, oracle = R.policy == kOracle;
     // materialisation statistics, accumulated as candidates are decided
@@ -1034,6 +1151,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     __syncwarp();
     // pass B: swap-ins, immediate swap-ins, denials, batch, in candidate order
     long long lsw = log0 + A.ne, limm = lsw + nsw, lden = limm + nimm;
+    const bool logging = (R.flags & kLogEvents) != 0;
     int bpos = 0;
     long long mv = 0;
     unsigned* bout = R.batch + (long long)i * R.n;
@@ -1073,8 +1191,13 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
                 sd = swap_latency(R.prof, c.z);
             }
         }
-        unsigned swm = __ballot_sync(FULL, sw), imm_m = __ballot_sync(FULL, imm),
-                 dnm = __ballot_sync(FULL, den), bm = __ballot_sync(FULL, inb);
+        // swap-in / immediate / denial masks only place log lines
+        unsigned swm = __ballot_sync(FULL, sw), bm = __ballot_sync(FULL, inb);
+        unsigned imm_m = 0, dnm = 0;
+        if (logging) {
+            imm_m = __ballot_sync(FULL, imm);
+            dnm = __ballot_sync(FULL, den);
+        }
         unsigned lt = lanemask_lt();
         if (sw) {
             unsigned m = R.rs[c.x].meta;
@@ -1413,6 +1536,9 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     const long long abase = R.n > 0 ? a.aoff[g] : 0;
     R.arrival = a.arrival + g;
     R.rec = a.rec + g;
+    R.ph = a.ph + g;
+    R.bpv = a.bpv + abase;
+    R.bpk = a.bpk + abase;
     R.dig = a.dig + abase;
     R.del = a.del + abase;
     R.qent = a.qent + d.queue_base;
@@ -1487,6 +1613,10 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
             R.spec[k] = a.spec[g + k];
             R.aoff[k] = a.aoff32[g + k];
         }
+        PacerHot zp;
+        zp.dlast = zp.dcur = zp.t0 = 0.0;
+        zp.nbp = zp.jn = 0;
+        R.ph[k] = zp;
         RecOut z;
         z.arrival = z.prefill_complete = z.reasoning_end = z.first_answer_delivery = 0.0;
         z.first_answer_iter_start = z.blocked = z.completion = z.mig_start = z.mig_end = 0.0;
@@ -1558,7 +1688,7 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     // outputs the metric kernels read: delivered counts and blocked totals
     for (int k = lane_id(); k < R.n; k += 32) {
         R.rec[k].blocked = R.blocked[k];
-        if (resident) a.rs[g + k].ndel = R.rs[k].ndel;
+        if (resident) a.rs[g + k] = R.rs[k];
     }
     if (lane_id() == 0) {
         ReplicaOut o;

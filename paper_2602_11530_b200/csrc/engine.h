@@ -112,6 +112,21 @@ struct __align__(16) ReqState {
     int cursor;       // digests known <= a past `now` (pacer health cursor)
 };
 
+// Pacer state of an answering request (PacerState, instance.hpp:22-39) in
+// breakpoint form. Digest k is d_k = max(gen_k, d_{k-1} + tpot) with d_0 =
+// gen_0 (instance.cpp:10-20); it equals gen_k only at "breakpoints" (the
+// first token and tokens generated after the pacing lead ran out) and is
+// d_{k-1} + tpot otherwise, so the digest sequence is stored as its
+// breakpoints {k, gen_k} (bpk / bpv arenas, ~3 per request on C2 instead of
+// one double per answer token) and replayed with the same double additions.
+struct __align__(16) PacerHot {
+    double dlast;  // d_{nd-1}: last digest (the QoE horizon at finish)
+    double dcur;   // d_{cursor-1}: last digest known <= a past `now`
+    double t0;     // first delivery (health's t0)
+    int nbp;       // breakpoints recorded
+    int jn;        // breakpoints consumed by the health cursor
+};
+
 // Batch-wide device arenas.
 struct Arena {
     const ReplicaDesc* desc;
@@ -127,7 +142,10 @@ struct Arena {
     ReqState* rs;     // per-request scheduling state (one 32-byte sector each)
     double* blocked;  // blocked_interval_total accumulator (global-resident replicas)
     RecOut* rec;
-    double* dig;      // digest times (always)
+    PacerHot* ph;     // per-request pacer state
+    double* bpv;      // digest breakpoint values (answer-slot arena)
+    int* bpk;         // digest breakpoint token indices (answer-slot arena)
+    double* dig;      // full digest times (kRecordDeliv)
     double* del;      // delivery times (kRecordDeliv)
     // queues / batches / events
     uint2* qent;      // {request index, enqueue_seq}

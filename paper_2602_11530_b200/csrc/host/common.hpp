@@ -156,6 +156,7 @@ Batch* batch_create(const std::vector<Job>& jobs);
 void batch_execute(Batch* b);
 void batch_summaries(Batch* b, std::vector<DeviceSummary>& out);
 void batch_free(Batch* b);
+void batch_rows(Batch* b, std::vector<std::vector<Row>>& rows);
 void batch_set_groups(Batch* b, const int* group_of_replica, int n_groups);
 void batch_histograms(Batch* b, unsigned long long* hist, unsigned long long* slo);
 

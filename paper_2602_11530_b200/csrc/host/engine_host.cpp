@@ -68,7 +68,12 @@ Shape pick_shape(int reps, int max_ni, int max_n) {
     cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     const int budget = std::max(48 * 1024, optin) - 1024;  // per CTA
     const int sm_budget = std::max(budget, per_sm_smem - 2048);
-    constexpr int kMaxWarpsPerSm = 16;  // 128 registers per thread
+    // Measured on C2 replicas (HBM/L2-resident request state): 8 warps per SM
+    // (unconstrained registers) beats 12 and 16 (register-capped variants
+    // spill around the out-of-line calls, and more concurrent replicas
+    // overflow L2); more replicas than warps are work-stolen.
+    const char* menv = std::getenv("PB_MAX_WARPS_PER_SM");
+    const int kMaxWarpsPerSm = menv ? std::max(1, std::min(16, std::atoi(menv))) : 8;
     const char* env = std::getenv("PB_SMEM");
     const int mode = env ? std::atoi(env) : -1;  // 0: HBM request state, 1: shared, -1: auto
     const char* henv = std::getenv("PB_SMEM_HEAP");  // test hook: tiny heap forces HBM spills
@@ -89,8 +94,15 @@ Shape pick_shape(int reps, int max_ni, int max_n) {
     const bool use_a = a_ok && (mode == 1 || warps_fit(pa) >= std::min(need_w, 4));
     Shape sh = use_a ? a : b;
     const int per_warp = use_a ? pa : pbw;
-    const int w = std::max(1, std::min(need_w, warps_fit(per_warp)));
-    sh.wpb = std::max(1, std::min({4, w, budget / per_warp}));
+    int w = std::max(1, std::min(need_w, warps_fit(per_warp)));
+    if (const char* wenv = std::getenv("PB_WARPS_PER_SM"))  // experiment hook
+        w = std::max(1, std::min(w, std::atoi(wenv)));
+    // warps per CTA: the divisor of the per-SM warp count that keeps all w
+    // warps resident (6 warps/SM = 2 CTAs of 3, not 1 CTA of 4)
+    const int wpb_max = std::max(1, std::min({4, w, budget / per_warp}));
+    sh.wpb = wpb_max;
+    for (int c = wpb_max - 1; c >= 1; --c)
+        if (c * (w / c) > sh.wpb * (w / sh.wpb)) sh.wpb = c;
     const int blocks_per_sm = std::max(1, w / sh.wpb);
     sh.blocks = std::max(1, std::min((reps + sh.wpb - 1) / sh.wpb, sms * blocks_per_sm));
     return sh;
@@ -144,6 +156,7 @@ public:
     void execute();
     void fetch_summaries(std::vector<DeviceSummary>& out);
     void fetch_single(RunOutputs& o, bool records, bool log);
+    void fetch_rows(std::vector<std::vector<Row>>& rows);
     void enable_log(long long cap) { log_cap_ = cap; }
     void enable_records() { records_ = true; }
     void build();
@@ -174,7 +187,9 @@ public:
     DevBuf<int> d_aoff32_;
     DevBuf<double> d_blocked_;
     DevBuf<pb::RecOut> d_rec_;
-    DevBuf<double> d_dig_, d_del_;
+    DevBuf<double> d_dig_, d_del_, d_bpv_;
+    DevBuf<int> d_bpk_;
+    DevBuf<pb::PacerHot> d_ph_;
     DevBuf<uint2> d_qent_;
     DevBuf<pb::HeapEnt> d_heap_;
     DevBuf<unsigned char> d_cstat_, d_slo_;
@@ -331,7 +346,10 @@ void Batch::build() {
     d_cstat_.ensure(rq);
     d_elist_.ensure(rq);
     d_stack_.ensure(rq);
-    d_dig_.ensure(ans);
+    d_ph_.ensure(rq);
+    d_bpv_.ensure(ans);
+    d_bpk_.ensure(ans);
+    d_dig_.ensure(records_ ? ans : 1);
     d_del_.ensure(records_ ? ans : 1);
     d_qent_.ensure(q);
     d_batch_.ensure(bt);
@@ -401,6 +419,9 @@ pb::Arena Batch::arena(bool oracle) const {
     a.blocked = d_blocked_.p;
     a.rs = d_rs_.p;
     a.rec = d_rec_.p;
+    a.ph = d_ph_.p;
+    a.bpv = d_bpv_.p;
+    a.bpk = d_bpk_.p;
     a.dig = d_dig_.p;
     a.del = d_del_.p;
     a.qent = d_qent_.p;
@@ -542,6 +563,40 @@ void Batch::fetch_single(RunOutputs& o, bool records, bool log) {
         if (ro.nlog > log_cap_) o.log.resize(0), o.capacity = -ro.nlog;  // caller retries
     }
 }
+
+// Per-request metric rows of every replica (trace order within a replica).
+void Batch::fetch_rows(std::vector<std::vector<Row>>& rows) {
+    const long long n = total_req_;
+    std::vector<double> ttft(n), ttfat(n), qoe(n), blk(n);
+    std::vector<unsigned char> slo(n);
+    auto down = [&](void* dst, const void* src, size_t b) {
+        if (b) ck(cudaMemcpy(dst, src, b, cudaMemcpyDeviceToHost), "d2h");
+    };
+    down(ttft.data(), d_ttft_.p, n * sizeof(double));
+    down(ttfat.data(), d_ttfat_.p, n * sizeof(double));
+    down(qoe.data(), d_qoe_.p, n * sizeof(double));
+    down(blk.data(), d_block_.p, n * sizeof(double));
+    down(slo.data(), d_slo_.p, n);
+    rows.assign(n_rep_, {});
+    long long g = 0;
+    for (int r = 0; r < n_rep_; ++r) {
+        const Trace& t = *jobs_[r].trace;
+        rows[r].resize(t.size());
+        for (size_t k = 0; k < t.size(); ++k, ++g) {
+            Row& w = rows[r][k];
+            w.id = t[k].id;
+            w.reasoning = t[k].reasoning;
+            w.answering = t[k].answering;
+            w.ttft = ttft[g];
+            w.ttfat = ttfat[g];
+            w.qoe = qoe[g];
+            w.slo = slo[g] != 0;
+            w.blocking = blk[g];
+        }
+    }
+}
+
+void batch_rows(Batch* b, std::vector<std::vector<Row>>& rows) { b->fetch_rows(rows); }
 
 Batch* batch_create(const std::vector<Job>& jobs) {
     auto* b = new Batch(jobs);

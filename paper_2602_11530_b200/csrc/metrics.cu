@@ -13,6 +13,8 @@
 
 #include <cuda_runtime.h>
 
+#include <climits>
+
 #include <cub/device/device_segmented_sort.cuh>
 
 #include "engine.h"
@@ -36,8 +38,9 @@ __global__ void capacity_kernel(ReplicaDesc* desc, const ReplicaOut* oout, const
 }
 
 __global__ void rows_kernel(const int* rid, const MetricParams* params, const int4* spec,
-                            const long long* aoff, const RecOut* rec, const double* dig,
-                            const ReqState* rs, RowArrays rows, long long total) {
+                            const long long* aoff, const RecOut* rec, const PacerHot* ph,
+                            const double* bpv, const int* bpk, const ReqState* rs,
+                            RowArrays rows, long long total) {
     long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= total) return;
     const MetricParams mp = params[rid[g]];
@@ -51,13 +54,24 @@ __global__ void rows_kernel(const int* rid, const MetricParams* params, const in
     int nd = rs[g].ndel;
     long long n = sp.z;
     if (n >= 1 && nd > 0) {
-        const double* d = dig + aoff[g];
+        const PacerHot p = ph[g];
+        const double* bv = bpv + aoff[g];
+        const int* bk = bpk + aoff[g];
         double t0 = r.first_answer_delivery;
-        double horizon = d[nd - 1];
+        double horizon = p.dlast;
         if (horizon > t0) {
-            double da = 0.0;
+            // digests replayed from their breakpoints (engine.h PacerHot)
+            double da = 0.0, d = 0.0;
+            int j = 0, kn = p.nbp > 0 ? bk[0] : INT_MAX;
             for (int k = 0; k < nd; ++k) {
-                double x = __dsub_rn(horizon, d[k]);
+                if (k == kn) {
+                    d = bv[j];
+                    ++j;
+                    kn = j < p.nbp ? bk[j] : INT_MAX;
+                } else {
+                    d = __dadd_rn(d, mp.tpot);
+                }
+                double x = __dsub_rn(horizon, d);
                 da = __dadd_rn(da, 0.0 < x ? x : 0.0);
             }
             double ea = 0.0;
@@ -215,7 +229,7 @@ int launch_metrics(const Arena& a, const MetricParams* params, const long long* 
     }
     if (total > 0) {
         rows_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(
-            rid, params, a.spec, a.aoff, a.rec, a.dig, a.rs, rows, total);
+            rid, params, a.spec, a.aoff, a.rec, a.ph, a.bpv, a.bpk, a.rs, rows, total);
         size_t bytes = *sort_tmp_bytes;
         if (cub::DeviceSegmentedSort::SortKeys(sort_tmp, bytes, rows.ttft, rows.ttft_sorted,
                                                (int)total, n_rep, seg, seg + 1,
