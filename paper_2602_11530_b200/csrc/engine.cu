@@ -31,6 +31,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 #include "engine.h"
 
@@ -386,7 +387,6 @@ struct HealthView {
     const uint2* qent;
     long long qcap;
     const int* lo_len;
-    int* healthy;
     ReqState* rs;
     const int4* spec;
     PacerHot* ph;
@@ -430,45 +430,106 @@ DEVI bool pacer_healthy(const HealthView& V, double now, int idx, int answering)
     return (long long)c >= expected - V.slack;
 }
 
-// t_i for every instance (instance.cpp:67-74): AND over low-queue Answering
-// members, into healthy[]. Returns the number of pacer evaluations. One
-// out-of-line copy serves arrivals and both phase-boundary sites.
-__device__ __noinline__ long long health_scan(const HealthView V, double now) {
-    long long checks = 0;
-    for (int i = 0; i < V.ni; ++i) {
-        const uint2* q = V.qent + (long long)(2 * i + 1) * V.qcap;
-        int len = V.lo_len[i];
-        bool ok = true;
-        for (int base = 0; base < len && ok; base += 32) {
-            int k = base + lane_id();
-            bool bad = false;
-            bool chk = false;
-            if (k < len) {
-                uint2 e = q[k];
-                int4 h = V.rs[e.x].h;
-                if ((unsigned)h.z == e.y) {
-                    unsigned m = V.rs[e.x].meta;
-                    if (m_phase(m) == PH_ANSWER) {
-                        chk = true;
-                        bad = !pacer_healthy(V, now, (int)e.x, V.spec[e.x].z);
-                    }
+// t_i of instance i (instance.cpp:67-74): AND over its low-queue Answering
+// members, stopping at the first unhealthy one. Adds the pacer evaluations
+// made to *checks.
+DEVI bool instance_healthy(const HealthView& V, double now, int i, long long* checks) {
+    const uint2* q = V.qent + (long long)(2 * i + 1) * V.qcap;
+    const int len = V.lo_len[i];
+    bool ok = true;
+    for (int base = 0; base < len && ok; base += 32) {
+        int k = base + lane_id();
+        bool bad = false;
+        bool chk = false;
+        if (k < len) {
+            uint2 e = q[k];
+            int4 h = V.rs[e.x].h;
+            if ((unsigned)h.z == e.y) {
+                unsigned m = V.rs[e.x].meta;
+                if (m_phase(m) == PH_ANSWER) {
+                    chk = true;
+                    bad = !pacer_healthy(V, now, (int)e.x, V.spec[e.x].z);
                 }
             }
-            checks += __popc(__ballot_sync(FULL, chk));
-            ok = __ballot_sync(FULL, bad) == 0;
         }
-        if (lane_id() == 0) V.healthy[i] = ok ? 1 : 0;
+        *checks += __popc(__ballot_sync(FULL, chk));
+        ok = __ballot_sync(FULL, bad) == 0;
     }
-    __syncwarp();
-    return checks;
+    return ok;
 }
 
-DEVI void compute_health(const Rep& R, Scal& S) {
+// Instance selection with the monitor snapshot evaluated lazily
+// (cluster.cpp:10-44,59-62, instance.cpp:59-76). "argmin over healthy
+// instances" is the first healthy instance in (key, id) order, so instances
+// are visited in that order and t_i is evaluated only until one is healthy —
+// the same choice as snapshotting every instance first; the pacer cursors it
+// advances are monotone caches. Keys are non-negative and below 2^54 (token
+// sums of < 2^26 requests of < 2^26 tokens), ids below 512, so (key, id)
+// packs into one u64 and a plain warp min is the argmin.
+//   SEL_M:         argmin m_i = gpu + cpu (baseline routing, no health)
+//   SEL_M_HEALTHY: argmin m_i over healthy instances, else over all (Alg. 1)
+//   SEL_ANSWER:    argmin r_i over healthy, else argmin r_i + a_i (Alg. 2)
+// One out-of-line copy serves arrivals and both phase-boundary sites.
+enum : int { SEL_M = 0, SEL_M_HEALTHY = 1, SEL_ANSWER = 2 };
+struct SelOut {
+    int id;
+    int pad;
+    long long checks;
+};
+__device__ __noinline__ SelOut select_instance(const HealthView V, double now, int mode,
+                                               const long long* gpu, const long long* cpu,
+                                               const int* hcount, const int* afresh,
+                                               unsigned* rejected) {
+    const unsigned long long NONE = ~0ull;
+    const int ni = V.ni;
+    SelOut o;
+    o.checks = 0;
+    o.pad = 0;
+    for (int w = lane_id(); w < (ni + 31) / 32; w += 32) rejected[w] = 0u;
+    __syncwarp();
+    auto key = [&](int i, int pass) -> long long {
+        if (mode == SEL_ANSWER)
+            return pass == 0 ? (long long)hcount[i] : (long long)hcount[i] + afresh[i];
+        return gpu[i] + cpu[i];
+    };
+    auto argmin = [&](int pass) -> unsigned long long {
+        unsigned long long best = NONE;
+        for (int base = 0; base < ni; base += 32) {
+            const int i = base + lane_id();
+            unsigned long long v = NONE;
+            if (i < ni && (pass == 1 || !((rejected[i >> 5] >> (i & 31)) & 1u)))
+                v = ((unsigned long long)key(i, pass) << 9) | (unsigned)i;
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                const unsigned long long y = __shfl_xor_sync(FULL, v, off);
+                v = y < v ? y : v;
+            }
+            best = v < best ? v : best;
+        }
+        return best;
+    };
+    if (mode != SEL_M) {
+        while (true) {  // pass 0: healthy instances in key order
+            const unsigned long long b = argmin(0);
+            if (b == NONE) break;
+            const int i = (int)(b & 511u);
+            if (instance_healthy(V, now, i, &o.checks)) {
+                o.id = i;
+                return o;
+            }
+            if (lane_id() == 0) rejected[i >> 5] |= 1u << (i & 31);
+            __syncwarp();
+        }
+    }
+    o.id = (int)(argmin(1) & 511u);
+    return o;
+}
+
+DEVI HealthView health_view(const Rep& R) {
     HealthView V;
     V.qent = R.qent;
     V.qcap = R.qcap;
     V.lo_len = R.s.lo_len;
-    V.healthy = R.s.healthy;
     V.rs = R.rs;
     V.spec = R.spec;
     V.ph = R.ph;
@@ -478,50 +539,13 @@ DEVI void compute_health(const Rep& R, Scal& S) {
     V.tpot = R.tpot;
     V.slack = R.slack;
     V.ni = R.ni;
-    S.health += health_scan(V, S.now);
+    return V;
 }
-
-// Instance selection (cluster.cpp:10-44,59-62), lowest key with ties to the
-// lowest id (argmin_by's strict '<' in id order). Keys are non-negative and
-// below 2^54 (token sums of < 2^26 requests of < 2^26 tokens), ids below 512,
-// so (key, id) packs into one u64 and a plain warp min is the argmin.
-//   SEL_M:         argmin m_i = gpu + cpu (baseline routing)
-//   SEL_M_HEALTHY: argmin m_i over healthy instances, else over all (Alg. 1)
-//   SEL_ANSWER:    argmin r_i over healthy, else argmin r_i + a_i (Alg. 2)
-enum : int { SEL_M = 0, SEL_M_HEALTHY = 1, SEL_ANSWER = 2 };
-__device__ __noinline__ int select_instance(int ni, int mode, const long long* gpu,
-                                            const long long* cpu, const int* hcount,
-                                            const int* afresh, const int* healthy) {
-    const unsigned long long NONE = ~0ull;
-    unsigned long long best = NONE;
-    for (int pass = (mode == SEL_M ? 1 : 0); pass < 2 && best == NONE; ++pass) {
-        for (int base = 0; base < ni; base += 32) {
-            const int i = base + lane_id();
-            unsigned long long v = NONE;
-            if (i < ni && (pass == 1 || healthy[i])) {
-                const long long k = mode == SEL_ANSWER
-                                        ? (pass == 0 ? (long long)hcount[i]
-                                                     : (long long)hcount[i] + afresh[i])
-                                        : gpu[i] + cpu[i];
-                v = ((unsigned long long)k << 9) | (unsigned)i;
-            }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                const unsigned long long y = __shfl_xor_sync(FULL, v, o);
-                v = y < v ? y : v;
-            }
-            best = v < best ? v : best;
-        }
-    }
-    return (int)(best & 511u);
-}
-DEVI int select_by_m(const Rep& R, bool health) {
-    return select_instance(R.ni, health ? SEL_M_HEALTHY : SEL_M, R.s.gpu, R.s.cpu, R.s.hcount,
-                           R.s.afresh, R.s.healthy);
-}
-DEVI int select_answering(const Rep& R) {
-    return select_instance(R.ni, SEL_ANSWER, R.s.gpu, R.s.cpu, R.s.hcount, R.s.afresh,
-                           R.s.healthy);
+DEVI int select_instance(const Rep& R, Scal& S, int mode) {
+    const SelOut o = select_instance(health_view(R), S.now, mode, R.s.gpu, R.s.cpu, R.s.hcount,
+                                     R.s.afresh, reinterpret_cast<unsigned*>(R.s.healthy));  // scratch bitmap
+    S.health += o.checks;
+    return o.id;
 }
 
 // ------------------------------------------------------------- handlers
@@ -544,8 +568,7 @@ DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
     int cur = m_owner(m);
     if (lane_id() == 0) dequeue_lane(R, idx, cur, m, h.w);
     __syncwarp();
-    compute_health(R, S);
-    int target = select_answering(R);
+    int target = select_instance(R, S, SEL_ANSWER);
     long long kv = h.x;
     // cluster.cpp:46-57
     bool migrate;
@@ -1029,10 +1052,12 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             // over 32 lanes cannot overflow
             const int contrib = fc ? (int)my_need : 0;
             int pin = contrib;
+            if (__ballot_sync(FULL, fc)) {  // all-denied rounds (the tail) skip the scan
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int y = __shfl_up_sync(FULL, pin, o);
-                if (ln >= o) pin += y;
+                for (int o = 1; o < 32; o <<= 1) {
+                    int y = __shfl_up_sync(FULL, pin, o);
+                    if (ln >= o) pin += y;
+                }
             }
             const bool stop_here = (fc && (long long)pin > F) || (sf && !simple_sf);
             const unsigned sm = __ballot_sync(FULL, stop_here);
@@ -1265,8 +1290,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
 DEVI int on_arrival(Rep& R, Scal& S, int idx) {
     if (lane_id() == 0) R.rec[idx].arrival = S.now;
     const bool pascal = R.policy == kPascal;
-    if (pascal) compute_health(R, S);
-    int dst = select_by_m(R, pascal);
+    int dst = select_instance(R, S, pascal ? SEL_M_HEALTHY : SEL_M);
     emit(R, S, kLArrival, dst, idx);
     int4 sp = R.spec[idx];
     bool high;
@@ -1743,6 +1767,8 @@ int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slot
             cudaSuccess)
             return 2;
     }
+    if (const char* cv = getenv("PB_CARVEOUT"))  // experiment hook: shared-memory carveout %
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
     kern<<<blocks, warps_per_block * 32, smem, (cudaStream_t)stream>>>(a, max_ni, n_smem, c_smem,
                                                                        h_slots);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;

@@ -87,7 +87,8 @@ Shape pick_shape(int reps, int max_ni, int max_n) {
     int pa = pb::smem_per_warp(max_ni, a.n_smem, a.c_smem, h_slots);
     bool a_ok = pa <= budget && mode != 0;
     // B: request state in HBM (L2-resident), small shared candidate scratch
-    Shape b{0, std::min(max_n, 512), 0, 0, h_slots};
+    const char* cenv = std::getenv("PB_CAND_SMEM");  // experiment hook: scratch slots
+    Shape b{0, std::min(max_n, cenv ? std::max(32, std::atoi(cenv)) : 512), 0, 0, h_slots};
     while (b.c_smem > 32 && pb::smem_per_warp(max_ni, 0, b.c_smem, h_slots) * 8 > sm_budget)
         b.c_smem /= 2;
     int pbw = pb::smem_per_warp(max_ni, 0, b.c_smem, h_slots);
