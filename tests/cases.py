@@ -153,3 +153,18 @@ def cfg_text(c) -> str:
     for k, v in c["profile"].items():
         lines.append(f"{k}={'inf' if (isinstance(v, float) and math.isinf(v)) else repr(float(v))}")
     return "\n".join(lines) + "\n"
+# "xlarge": records + report files only (decision logs of 25 M+ lines are not
+# materialised). C3 = BASELINE.json configs[2] (ablation, 8 instances, 20k
+# requests) at lambda 8, capacity 0.9: Pascal, Pascal(NoMigration), FCFS; and a
+# C4-shaped run (configs[3]: CLI mixed preset, 64 instances, long reasoning
+# tail) scaled to 20k requests so the CPU reference finishes in seconds.
+# (NonAdaptive at this point runs > 15 CPU-minutes on the reference: its
+# queues grow without bound; it is covered by the medium ablation cases.)
+for name, pol, extra in (("pascal", "pascal", {}), ("nomig", "pascal", {"no_migration": 1}),
+                         ("fcfs", "fcfs", {})):
+    CASES.append(case(f"c3_l8_{name}", gen(20000, 8.0, CHAT, 1), pol, size="xlarge",
+                      instance_count=8, capacity_fraction=0.9, **extra))
+CASES.append(case("c4s_pascal", cli_mixed(20000, 16.0, 1), "pascal", size="xlarge",
+                  instance_count=64, capacity_fraction=0.9))
+CASES.append(case("c4s_fcfs", cli_mixed(20000, 16.0, 1), "fcfs", size="xlarge",
+                  instance_count=64, capacity_fraction=0.9))

@@ -61,3 +61,24 @@ def test_large_bit_exact(c, tmp_path):
     pb.run(t, make_profile(c), make_cfg(c), prefix)
     for ext, want in g["report"].items():
         assert sha_file(f"{prefix}.{ext}") == want, ext
+
+
+XLARGE = [c for c in CASES if c["name"] in GOLD and c["size"] == "xlarge"]
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("c", XLARGE, ids=[c["name"] for c in XLARGE])
+def test_xlarge_records_and_reports(c, tmp_path):
+    """C3 (BASELINE.json configs[2]: 20k requests, 8 instances) and a
+    C4-shaped 64-instance run: every RequestRecord double and every report
+    byte equal to the reference's (decision logs not materialised)."""
+    g = GOLD[c["name"]]
+    t = build_trace(c["trace"])
+    rec = str(tmp_path / "gpu.rec")
+    pb.run_dump(t, make_profile(c), make_cfg(c), rec, None)
+    assert sha_file(rec) == g["records"]
+    prefix = str(tmp_path / "rep")
+    pb.run(t, make_profile(c), make_cfg(c), prefix)
+    for ext, want in g["report"].items():
+        assert sha_file(f"{prefix}.{ext}") == want, ext
