@@ -144,7 +144,6 @@ CASES.append(case("c2_pascal", gen(2000, 12.0, CHAT, 1), "pascal", size="large",
 CASES.append(case("c2_fcfs", gen(2000, 12.0, CHAT, 1), "fcfs", size="large",
                   instance_count=4, capacity_fraction=0.3))
 
-BY_NAME = {c["name"]: c for c in CASES}
 
 
 def cfg_text(c) -> str:
@@ -168,3 +167,5 @@ CASES.append(case("c4s_pascal", cli_mixed(20000, 16.0, 1), "pascal", size="xlarg
                   instance_count=64, capacity_fraction=0.9))
 CASES.append(case("c4s_fcfs", cli_mixed(20000, 16.0, 1), "fcfs", size="xlarge",
                   instance_count=64, capacity_fraction=0.9))
+
+BY_NAME = {c["name"]: c for c in CASES}
