@@ -1667,11 +1667,13 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     S.adm_rounds = S.adm_slow = 0;
     const long long heap_cap = (long long)R.n + R.ni + 1;
 
+    // the next arrival time is loaded one event ahead
+    double ta_next = R.n > 0 ? R.arrival[0] : 0.0;
     while (S.status == 0) {
         const bool has_arr = S.next_arr < R.n;
         const bool has_ev = S.hn > 0;
         if (!has_arr && !has_ev) break;
-        double ta = has_arr ? R.arrival[S.next_arr] : 0.0;
+        const double ta = ta_next;
         HeapEnt top;
         top.t = 0.0;
         top.key = 0;
@@ -1684,6 +1686,7 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
             et = ta;
             kind = 0;
             id = (unsigned)S.next_arr++;
+            if (S.next_arr < R.n) ta_next = R.arrival[S.next_arr];
         } else {
             HeapEnt e = heap_pop(R, S);
             et = e.t;

@@ -13,7 +13,7 @@ from harness import (build_trace, first_diff, golden, make_cfg, make_profile, or
                      sha_file)
 
 GOLD = golden()
-PARAMS = [c for c in CASES if c["name"] in GOLD and c["size"] != "large"]
+PARAMS = [c for c in CASES if c["name"] in GOLD and c["size"] not in ("large", "xlarge")]
 
 
 @pytest.mark.gpu
