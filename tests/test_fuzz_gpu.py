@@ -1,0 +1,111 @@
+"""Randomised parity: seeded random traces × random run configs × random
+latency profiles, GPU engine vs the REAL reference (oracle/_ref/ref_dump =
+/root/reference/proj compiled unmodified, built here and shipped with the
+repo). Records (every double, hex) and the pascal-events-v1 decision log
+must be byte-identical. The generator explores corners the fixed cases do not
+combine: tiny quanta, low demotion thresholds, pacer slack, explicit
+capacities, infinite or slow swap/fabric bandwidth, preloaded KV, R = 0 /
+A = 1 requests, many instances, and every policy / ablation."""
+import math
+import os
+import random
+import subprocess
+
+import pytest
+
+import paper_2602_11530_b200 as pb
+from cases import cfg_text
+from harness import REF_DUMP, build_trace, first_diff, make_cfg, make_profile
+
+N_CASES = 256
+SEED = 20261017
+
+
+def random_case(rng: random.Random, k: int):
+    n = rng.choice([1, 2, 5, 17, 40, 80, 150])
+    rate = rng.choice([1.5, 6.0, 14.0, 40.0])
+    dist = rng.choice([
+        ("uniform:64:512", "uniform:0:600", "uniform:1:300"),
+        ("constant:128", "constant:0", "uniform:1:64"),
+        ("uniform:16:64", "hist:0=0.2,128=0.5,1024=0.3", "constant:1"),
+        ("uniform:64:512", "hist:256=0.35,512=0.30,768=0.20,1024=0.10,1536=0.04,2048=0.01",
+         "uniform:256:1024"),
+    ])
+    trace = {"gen": [n, rate, *dist, 1000 + k, rng.random() < 0.2]}
+    if rng.random() < 0.3:
+        other = {"gen": [n, rate, "uniform:64:512", "uniform:200:2000", "uniform:1:200",
+                         2000 + k, rng.random() < 0.3]}
+        trace = {"mix": [trace, other, rng.choice([0.25, 0.5]), 3000 + k]}
+    policy = rng.choice(["fcfs", "rr", "oracle", "pascal", "pascal", "pascal"])
+    cfg = {"policy": policy, "instance_count": rng.choice([1, 1, 2, 3, 4, 6])}
+    if rng.random() < 0.2:
+        cfg["gpu_capacity"] = rng.choice([600, 2000, 5000])
+    else:
+        cfg["capacity_fraction"] = rng.choice([0.15, 0.3, 0.5, 0.8, 1.0])
+    cfg["token_quantum"] = rng.choice([1, 7, 50, 500])
+    cfg["demotion_threshold"] = rng.choice([100, 700, 5000])
+    cfg["pacer_slack_tokens"] = rng.choice([0, 0, 2, 10])
+    cfg["target_tpot"] = rng.choice([0.02, 0.1, 0.3])
+    if policy == "pascal":
+        ab = rng.random()
+        if ab < 0.2:
+            cfg["no_migration"] = 1
+        elif ab < 0.4:
+            cfg["non_adaptive"] = 1
+    prof = {"decode_base": rng.choice([0.0003, 0.005, 0.03]),
+            "decode_per_request": rng.choice([0.0, 0.001]),
+            "decode_per_kv_token": rng.choice([0.0, 1e-6]),
+            "prefill_per_token": rng.choice([0.0, 0.00005, 0.00025]),
+            "swap_bandwidth": rng.choice([math.inf, 51200.0, 2000.0]),
+            "fabric_bandwidth": rng.choice([51200.0, 5000.0]),
+            "fabric_latency": rng.choice([0.0, 0.002])}
+    return {"name": f"fuzz{k}", "trace": trace, "cfg": cfg, "profile": prof, "size": "small"}
+
+
+RNG = random.Random(SEED)
+FUZZ = [random_case(RNG, k) for k in range(N_CASES)]
+# Some draws land in an evict / swap-in thrash regime (slow swaps, tiny
+# quanta, tight capacity) where the reference itself runs for minutes or
+# more; a draw whose reference run exceeds REF_BUDGET_S is skipped, not run.
+REF_BUDGET_S = 10.0
+
+
+def ref_run(c, t, tmp):
+    hexp = os.path.join(tmp, "t.hex")
+    t.save_hex(hexp)
+    cfgp = os.path.join(tmp, "c.cfg")
+    with open(cfgp, "w") as f:
+        f.write(cfg_text(c))
+    rec, ev = os.path.join(tmp, "ref.rec"), os.path.join(tmp, "ref.ev")
+    try:
+        r = subprocess.run([REF_DUMP, "run", hexp, cfgp, rec, ev], capture_output=True,
+                           text=True, timeout=REF_BUDGET_S)
+    except subprocess.TimeoutExpired:
+        pytest.skip(f"reference exceeds {REF_BUDGET_S:.0f} s on this draw (thrash regime)")
+    return r, rec, ev
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c", FUZZ, ids=[c["name"] for c in FUZZ])
+def test_fuzz_bit_exact_vs_reference(c, tmp_path):
+    if not os.path.exists(REF_DUMP):
+        pytest.skip("reference not built (oracle/_ref)")
+    t = build_trace(c["trace"])
+    r, rrec, rev = ref_run(c, t, str(tmp_path))
+    grec, gev = str(tmp_path / "gpu.rec"), str(tmp_path / "gpu.ev")
+    if r.returncode != 0:  # the reference rejects / fails: so must we, same status class
+        with pytest.raises(pb.PascalError):
+            pb.run_dump(t, make_profile(c), make_cfg(c), grec, gev)
+        return
+    pb.run_dump(t, make_profile(c), make_cfg(c), grec, gev)
+    for a, b in ((grec, rrec), (gev, rev)):
+        if open(a, "rb").read() != open(b, "rb").read():
+            pytest.fail(f"{c}\n" + first_diff(a, b))
+
+
+def test_fuzz_cases_are_reproducible():
+    again = random.Random(SEED)
+    assert [random_case(again, k) for k in range(N_CASES)] == FUZZ
+    assert len({repr(c["cfg"]) for c in FUZZ}) > N_CASES // 2
+    pols = {c["cfg"]["policy"] for c in FUZZ}
+    assert pols == {"fcfs", "rr", "oracle", "pascal"}
