@@ -190,8 +190,14 @@ Trace mix(const Trace& base, const Trace& repl, double fraction, std::uint64_t s
 }
 
 void check_trace(const Trace& t) {
+    // duplicate-id check: a bitmap when ids are small (generated traces use
+    // 0..n-1), a hash set otherwise
+    long max_id = -1;
+    for (const Spec& s : t) max_id = std::max(max_id, s.id);
+    const bool dense = max_id < 4 * (long)t.size() + 64;
+    std::vector<unsigned char> seen_bits(dense ? (size_t)(max_id + 1) : 0, 0);
     std::unordered_set<long> seen;
-    seen.reserve(t.size() * 2);
+    if (!dense) seen.reserve(t.size() * 2);
     double last_arrival = -1.0;
     long last_id = -1;
     for (const Spec& s : t) {
@@ -203,7 +209,7 @@ void check_trace(const Trace& t) {
         if (s.prompt < 1) bad("prompt_tokens must be >= 1");
         if (s.reasoning < 0) bad("reasoning_tokens must be >= 0");
         if (s.answering < 1) bad("answering_tokens must be >= 1");
-        if (!seen.insert(s.id).second) bad("duplicate id");
+        if (dense ? seen_bits[(size_t)s.id]++ != 0 : !seen.insert(s.id).second) bad("duplicate id");
         if (s.arrival < last_arrival || (s.arrival == last_arrival && s.id < last_id))
             bad("trace not sorted by (arrival_time, id)");
         last_arrival = s.arrival;
