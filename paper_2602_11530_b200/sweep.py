@@ -157,3 +157,146 @@ def reduce_results(summaries, hist, slo, group=None, device=None):
     dist.all_reduce(h, group=group)
     dist.all_reduce(s, group=group)
     return allsum, h, s
+
+
+# ------------------------------------------------------------------ driver
+def select_ids(seeds: int, rates: Sequence[int], policies: Sequence[int]) -> List[int]:
+    """Replica ids of the (seed < seeds) x rates x policies sub-grid, ascending."""
+    rs, ps = set(rates), set(policies)
+    out = []
+    for seed in range(seeds):
+        for k in range(N_RATES):
+            if k not in rs:
+                continue
+            for p in range(len(POLICY_VARIANTS)):
+                if p in ps:
+                    out.append((seed * N_RATES + k) * len(POLICY_VARIANTS) + p)
+    return out
+
+
+def run_c5(seeds: int = 4096, rates: Sequence[int] = range(N_RATES),
+           policies: Sequence[int] = range(len(POLICY_VARIANTS)), chunk: int = 4736,
+           device: int = 0, progress=None):
+    """The C5 replica sweep (BASELINE.json configs[4]) on this rank's shard:
+    one process per GPU (torch.distributed initialised by the caller, NCCL on
+    the GPU box), replicas in device batches of `chunk`, then the end-of-sweep
+    exchange (all-gather of per-replica summaries, all-reduce of the
+    per-(rate, policy) TTFT histograms and SLO counters). Returns
+    (global summaries [n, len(SUMMARY_FIELDS)], histograms, slo, device_ms of
+    this rank)."""
+    import torch
+    import torch.distributed as dist
+
+    from . import api
+
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    ids = select_ids(seeds, rates, policies)
+    weights = [policy_cost(replica_params(r)[2]) for r in ids]
+    mine = [ids[j] for j in shard(len(ids), world, rank, weights)]
+    api.set_device(device)
+    rows = []
+    hist = torch.zeros((n_groups(), HIST_BINS + 2), dtype=torch.int64)
+    slo = torch.zeros((n_groups(), 2), dtype=torch.int64)
+    device_ms = 0.0
+    for lo in range(0, len(mine), chunk):
+        part = mine[lo:lo + chunk]
+        traces, profs, cfgs = [], [], []
+        for r in part:
+            recipe, cfg, prof = replica_recipe(r)
+            traces.append(_trace(recipe))
+            cfgs.append(api.run_config(**cfg))
+            profs.append(api.Profile.default(**prof))
+        b = api.Batch(traces, profs, cfgs)
+        b.set_groups([group_of(r) for r in part], n_groups())
+        b.execute()
+        device_ms += api.last_timing().total_ms
+        summ = b.summaries()
+        h, s = b.histograms()
+        hist += torch.tensor(h, dtype=torch.int64)
+        slo += torch.tensor(s, dtype=torch.int64)
+        for r, x in zip(part, summ):
+            rows.append([float(r), x.ttft_mean, x.ttft_p50, x.ttft_p99, x.slo_violation_rate,
+                         x.throughput, float(x.requests), float(x.request_iterations),
+                         float(x.status)])
+        del b
+        if progress:
+            progress(lo + len(part), len(mine))
+    t = torch.tensor(rows, dtype=torch.float64).reshape(-1, len(SUMMARY_FIELDS))
+    if world > 1:
+        dev = torch.device("cuda", device)
+        allrows, h, s = reduce_results(t.to(dev), hist.to(dev), slo.to(dev))
+        return allrows.cpu(), h.cpu(), s.cpu(), device_ms
+    return t, hist, slo, device_ms
+
+
+def _trace(recipe):
+    from . import api
+
+    if "gen" in recipe:
+        n, rate, pd, rd, ad, seed, pre = recipe["gen"]
+        return api.Trace.generate(n, rate, pd, rd, ad, seed, pre)
+    base, repl, frac, seed = recipe["mix"]
+    return api.Trace.mix(_trace(base), _trace(repl), frac, seed)
+
+
+def group_table(hist, slo) -> List[dict]:
+    """Per-(rate, policy) rows: TTFT P50/P99 read off the device histogram,
+    SLO-violation rate from the counters."""
+    out = []
+    for g in range(n_groups()):
+        k, p = divmod(g, len(POLICY_VARIANTS))
+        counts = [int(x) for x in hist[g]]
+        n = int(slo[g][1])
+        if n == 0:
+            continue
+        out.append({"rate": rate_of(k), "policy": POLICY_VARIANTS[p][0],
+                    "requests": n, "slo_violation_rate": int(slo[g][0]) / n,
+                    "ttft_p50_hist": percentile_from_hist(counts, 0.5),
+                    "ttft_p99_hist": percentile_from_hist(counts, 0.99)})
+    return out
+
+
+def main(argv=None) -> int:
+    """python -m paper_2602_11530_b200.sweep [--seeds S] [--rates K..] [--out CSV]
+    (under torchrun for several GPUs: one rank per GPU)."""
+    import argparse
+    import os
+
+    import torch.distributed as dist
+
+    ap = argparse.ArgumentParser(description="C5 replica sweep (seeds x rates x policies)")
+    ap.add_argument("--seeds", type=int, default=64)
+    ap.add_argument("--rates", type=int, nargs="+", default=list(range(3, N_RATES)),
+                    help="rate indices k (lambda = 2^(k/3)); k < 3 are thrash regimes")
+    ap.add_argument("--policies", type=int, nargs="+", default=list(range(len(POLICY_VARIANTS))))
+    ap.add_argument("--chunk", type=int, default=4736)
+    ap.add_argument("--out", default="c5_sweep.csv")
+    a = ap.parse_args(argv)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    rows, hist, slo, ms = run_c5(a.seeds, a.rates, a.policies, a.chunk, local)
+    if not dist.is_initialized() or dist.get_rank() == 0:
+        with open(a.out, "w") as f:
+            f.write("rate,policy,requests,slo_violation_rate,ttft_p50_hist,ttft_p99_hist\n")
+            for r in group_table(hist, slo):
+                f.write(f"{r['rate']:.6f},{r['policy']},{r['requests']},"
+                        f"{r['slo_violation_rate']:.6f},{r['ttft_p50_hist']:.6g},"
+                        f"{r['ttft_p99_hist']:.6g}\n")
+        bad = int((rows[:, 8] != 0).sum()) if rows.numel() else 0
+        print(f"{rows.shape[0]} replicas, {int(rows[:, 7].sum()) if rows.numel() else 0} "
+              f"request-iterations, device {ms / 1e3:.2f} s on rank 0, failures {bad}; "
+              f"wrote {a.out}")
+    if dist.is_initialized():
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

@@ -79,3 +79,46 @@ def test_replica_ids_round_trip():
     hist[100] = 1
     assert sweep.percentile_from_hist(hist, 0.5) == sweep.hist_edges()[10]
     assert sweep.percentile_from_hist(hist, 1.0) == sweep.hist_edges()[100]
+
+
+def test_select_ids_and_group_table():
+    ids = sweep.select_ids(3, [3, 15], [0, 3])
+    assert len(ids) == 3 * 2 * 2 and ids == sorted(ids)
+    assert {sweep.replica_params(r)[1] for r in ids} == {3, 15}
+    assert {sweep.replica_params(r)[2] for r in ids} == {0, 3}
+    hist = torch.zeros((sweep.n_groups(), sweep.HIST_BINS + 2), dtype=torch.int64)
+    slo = torch.zeros((sweep.n_groups(), 2), dtype=torch.int64)
+    g = sweep.group_of(ids[0])
+    hist[g, 20] = 10
+    slo[g] = torch.tensor([3, 10])
+    rows = sweep.group_table(hist, slo)
+    assert len(rows) == 1 and rows[0]["policy"] == "pascal" and rows[0]["rate"] == 2.0
+    assert rows[0]["slo_violation_rate"] == 0.3
+    assert rows[0]["ttft_p99_hist"] == sweep.hist_edges()[20]
+
+
+@pytest.mark.gpu
+def test_c5_subgrid_matches_reference(tmp_path):
+    """run_c5 on 2 seeds x 2 rates x 4 policies: every replica's P99 TTFT,
+    SLO-violation rate and mean TTFT equal the reference's (oracle/_ref)."""
+    import subprocess
+
+    from cases import cfg_text
+    from harness import REF_DUMP, build_trace
+
+    if not os.path.exists(REF_DUMP):
+        pytest.skip("reference not built")
+    rows, hist, slo, _ = sweep.run_c5(seeds=2, rates=[4, 12], chunk=5)
+    assert rows.shape[0] == 16 and int((rows[:, 8] != 0).sum()) == 0
+    assert int(slo[:, 1].sum()) == 16 * 256
+    for row in rows.tolist():
+        recipe, cfg, prof = sweep.replica_recipe(int(row[0]))
+        t = build_trace(recipe)
+        hexp, cfgp = str(tmp_path / "t.hex"), str(tmp_path / "c.cfg")
+        t.save_hex(hexp)
+        with open(cfgp, "w") as f:
+            f.write(cfg_text({"cfg": cfg, "profile": prof}))
+        out = subprocess.run([REF_DUMP, "sim", hexp, cfgp], check=True, capture_output=True,
+                             text=True, timeout=300).stdout.split()
+        p99, slo_rate, mean = (float.fromhex(x) for x in out[1:4])
+        assert (row[3], row[4], row[1]) == (p99, slo_rate, mean), row
