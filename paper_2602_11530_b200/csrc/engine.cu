@@ -159,6 +159,7 @@ struct Rep {
     int4* spec;
     int* aoff;  // answer-slot offset relative to dig / del
     ReqState* rs;
+    double* blocked;
     RecOut* rec;
     PacerHot* ph;
     double* bpv;  // this replica's breakpoint arenas (indexed by aoff)
@@ -403,15 +404,14 @@ struct HealthView {
 // d_c is the next breakpoint's value when its token index is c, else
 // d_{c-1} + tpot — the reference's own addition.
 DEVI bool pacer_healthy(const HealthView& V, double now, int idx, int answering) {
-    PacerHot p = V.ph[idx];
-    const int nd = p.ndel;
+    int nd = V.rs[idx].ndel;
     if (nd == 0) return true;
-    const int off = V.aoff[idx];
-    const double t0 = V.bpv[off];  // breakpoint 0 = the first delivery
-    long long expected = 1 + (long long)floor(__ddiv_rn(__dsub_rn(now, t0), V.tpot));
+    PacerHot p = V.ph[idx];
+    long long expected = 1 + (long long)floor(__ddiv_rn(__dsub_rn(now, p.t0), V.tpot));
     if (expected > answering) expected = answering;
-    int c = p.cursor;
+    int c = V.rs[idx].cursor;
     if (c < nd) {
+        const int off = V.aoff[idx];
         const int c0 = c;
         while (c < nd) {
             const bool isbp = p.jn < p.nbp && V.bpk[off + p.jn] == c;
@@ -422,7 +422,7 @@ DEVI bool pacer_healthy(const HealthView& V, double now, int idx, int answering)
             if (isbp) ++p.jn;
         }
         if (c != c0) {
-            V.ph[idx].cursor = c;
+            V.rs[idx].cursor = c;
             V.ph[idx].dcur = p.dcur;
             V.ph[idx].jn = p.jn;
         }
@@ -616,14 +616,15 @@ DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
 // engine.cpp:148-156); shared by the R == 0 path of prefill completion.
 // Records a breakpoint when the digest is the generation time itself.
 DEVI void deliver_lane(const Rep& R, double now, int idx, double iter_start) {
-    PacerHot* pp = R.ph + idx;
-    const int nd = pp->ndel;
+    int nd = R.rs[idx].ndel;
     const int off = R.aoff[idx];
+    PacerHot* pp = R.ph + idx;
     double v;
     bool bp;
     if (nd == 0) {
         v = now;
         bp = true;
+        pp->t0 = now;
     } else {
         const double x = __dadd_rn(pp->dlast, R.tpot);
         bp = !(now < x);  // std::max(gen, prev + tpot) picks gen
@@ -636,11 +637,11 @@ DEVI void deliver_lane(const Rep& R, double now, int idx, double iter_start) {
         pp->nbp = j + 1;
     }
     pp->dlast = v;
-    pp->ndel = nd + 1;
     if (R.flags & kRecordDeliv) {
         R.dig[off + nd] = v;
         R.del[off + nd] = now;
     }
+    R.rs[idx].ndel = nd + 1;
     if (nd == 0) {
         R.rec[idx].first_answer_delivery = now;
         R.rec[idx].first_answer_iter_start = iter_start;
@@ -1108,10 +1109,6 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         if (valid) R.cstat[ci_l] = st;
         // statistics for this (now final) chunk
         const bool adm = st == CS_ADMIT, den = st == CS_DENY;
-        if (!__ballot_sync(FULL, adm)) {  // all-denied chunk (the swapped-out tail)
-            nden += __popc(__ballot_sync(FULL, den));
-            continue;
-        }
         bool wt = false, inb = false, sw = false, imm = false;
         if (adm) {
             if (my_w & CF_WAIT) wt = true;
@@ -1191,7 +1188,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     if (lane_id() < n) {
         c_n = R.cand[lane_id()];
         st_n = R.cstat[lane_id()];
-        if (st_n == CS_DENY) bl_n = R.rs[c_n.x].blocked;
+        if (st_n == CS_DENY) bl_n = R.blocked[c_n.x];
     }
     for (int base = 0; base < n; base += 32) {
         int k = base + lane_id();
@@ -1201,16 +1198,12 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         if (k + 32 < n) {
             c_n = R.cand[k + 32];
             st_n = R.cstat[k + 32];
-            bl_n = st_n == CS_DENY ? R.rs[c_n.x].blocked : 0.0;
+            bl_n = st_n == CS_DENY ? R.blocked[c_n.x] : 0.0;
         }
         bool adm = false, den = false, inb = false, sw = false, imm = false;
         if (k < n) {
             adm = st_c == CS_ADMIT;
             den = st_c == CS_DENY;
-        }
-        if (!logging && !__ballot_sync(FULL, adm)) {  // all-denied chunk: blocked time only
-            if (den) R.rs[c.x].blocked = __dadd_rn(bl, dur);
-            continue;
         }
         double sd = 0.0;
         if (adm && !(c.w & CF_WAIT)) {
@@ -1242,7 +1235,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             log_put(R, limm + __popc(imm_m & lt), S.now, kLSwapIn, i, c.x, 0);
         }
         if (den) {
-            R.rs[c.x].blocked = __dadd_rn(bl, dur);
+            R.blocked[c.x] = __dadd_rn(bl, dur);
             log_put(R, lden + __popc(dnm & lt), S.now, kLBlock, i, c.x, 0);
         }
         if (inb && kind == 2) bout[bpos + __popc(bm & lt)] = (unsigned)c.x;
@@ -1603,10 +1596,12 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     if (resident) {
         R.rs = reinterpret_cast<ReqState*>(sp);
         R.spec = reinterpret_cast<int4*>(R.rs + n_smem);
-        R.aoff = reinterpret_cast<int*>(R.spec + n_smem);
+        R.blocked = reinterpret_cast<double*>(R.spec + n_smem);
+        R.aoff = reinterpret_cast<int*>(R.blocked + n_smem);
     } else {
         R.rs = a.rs + g;
         R.spec = const_cast<int4*>(a.spec) + g;
+        R.blocked = a.blocked + g;
         R.aoff = const_cast<int*>(a.aoff32) + g;
     }
     sp += smem_req_bytes(n_smem);
@@ -1634,15 +1629,17 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
         z0.h = make_int4(0, 0, 0, 0);
         z0.meta = m_set_phase(0u, PH_WAIT);
         z0.qused = 0;
-        z0.blocked = 0.0;
+        z0.ndel = 0;
+        z0.cursor = 0;
         R.rs[k] = z0;
+        R.blocked[k] = 0.0;
         if (resident) {
             R.spec[k] = a.spec[g + k];
             R.aoff[k] = a.aoff32[g + k];
         }
         PacerHot zp;
-        zp.dlast = zp.dcur = 0.0;
-        zp.nbp = zp.jn = zp.ndel = zp.cursor = 0;
+        zp.dlast = zp.dcur = zp.t0 = 0.0;
+        zp.nbp = zp.jn = 0;
         R.ph[k] = zp;
         RecOut z;
         z.arrival = z.prefill_complete = z.reasoning_end = z.first_answer_delivery = 0.0;
@@ -1717,7 +1714,7 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     if (S.status == 0 && S.done != R.n) S.status = kErrStall;
     // outputs the metric kernels read: delivered counts and blocked totals
     for (int k = lane_id(); k < R.n; k += 32) {
-        R.rec[k].blocked = R.rs[k].blocked;
+        R.rec[k].blocked = R.blocked[k];
         if (resident) a.rs[g + k] = R.rs[k];
     }
     if (lane_id() == 0) {

@@ -101,15 +101,15 @@ enum LogKind : int {
     kLTransferComplete
 };
 
-// Mutable per-request scheduling state, packed into one 32-byte sector: the
-// queue scan (gather) reads it and a denial's blocked-time update writes the
-// same sector, so the planner touches one sector per candidate
-// (RequestState, proj/include/pascalsim/instance.hpp:41-62).
+// Mutable per-request scheduling state, packed into one 32-byte sector so a
+// queue scan touches one sector per request (RequestState,
+// proj/include/pascalsim/instance.hpp:41-62).
 struct __align__(16) ReqState {
     int4 h;           // {kv_tokens, tokens_generated, enqueue_seq (0 = not queued), quanta_exhausted}
     unsigned meta;    // phase:2 | loc:2 | swin:1 | swout:1 | qlow:1 | owner:16 (<<8)
     int qused;        // quantum_used_in_round
-    double blocked;   // blocked_interval_total (engine.cpp:229-232)
+    int ndel;         // delivered answer tokens
+    int cursor;       // digests known <= a past `now` (pacer health cursor)
 };
 
 // Pacer state of an answering request (PacerState, instance.hpp:22-39) in
@@ -119,14 +119,12 @@ struct __align__(16) ReqState {
 // d_{k-1} + tpot otherwise, so the digest sequence is stored as its
 // breakpoints {k, gen_k} (bpk / bpv arenas, ~3 per request on C2 instead of
 // one double per answer token) and replayed with the same double additions.
-// t0 (the first delivery) is breakpoint 0.
 struct __align__(16) PacerHot {
-    double dlast;  // d_{ndel-1}: last digest (the QoE horizon at finish)
+    double dlast;  // d_{nd-1}: last digest (the QoE horizon at finish)
     double dcur;   // d_{cursor-1}: last digest known <= a past `now`
+    double t0;     // first delivery (health's t0)
     int nbp;       // breakpoints recorded
     int jn;        // breakpoints consumed by the health cursor
-    int ndel;      // delivered answer tokens
-    int cursor;    // digests known <= a past `now` (pacer health cursor)
 };
 
 // Batch-wide device arenas.
@@ -142,6 +140,7 @@ struct Arena {
     const int* aoff32;      // same, relative to the replica's first request
     // mutable request state
     ReqState* rs;     // per-request scheduling state (one 32-byte sector each)
+    double* blocked;  // blocked_interval_total accumulator (global-resident replicas)
     RecOut* rec;
     PacerHot* ph;     // per-request pacer state
     double* bpv;      // digest breakpoint values (answer-slot arena)
@@ -198,13 +197,13 @@ struct RowArrays {
 #endif
 
 // Dynamic shared memory per warp: instance state for ni instances; for
-// replicas with n <= n_smem also the hot per-request state (52 B each:
-// ReqState 32, spec 16, answer offset 4) and
+// replicas with n <= n_smem also the hot per-request state (60 B each: hot,
+// spec, blocked, meta, quantum_used, delivered, cursor, answer offset) and
 // the event heap (n + ni + 2 entries of 16 B); and a candidate scratch of
 // c_smem entries (37 B each). Larger replicas keep request state and heap in
 // HBM; plans with more queued requests than c_smem use the HBM scratch.
 PB_HD inline int smem_inst_bytes(int ni) { return ((ni * 64 + 16) + 15) / 16 * 16; }
-PB_HD inline int smem_req_bytes(int n_smem) { return (n_smem * 52 + 15) / 16 * 16; }  // rs 32 + spec 16 + aoff 4
+PB_HD inline int smem_req_bytes(int n_smem) { return (n_smem * 60 + 15) / 16 * 16; }  // rs 32 + spec 16 + blocked 8 + aoff 4
 // Shared-memory event heap: sized for every pending event of a resident
 // replica; HBM-resident replicas start with h_slots slots (default 128) and
 // move their heap to HBM if it ever grows past them.

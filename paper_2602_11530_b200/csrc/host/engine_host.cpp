@@ -255,6 +255,7 @@ public:
     DevBuf<long long> d_aoff_, d_biggest_, d_echo_, d_seg_;
     DevBuf<unsigned> d_batch_, d_tmpq_, d_elist_, d_stack_;
     DevBuf<int> d_aoff32_;
+    DevBuf<double> d_blocked_;
     DevBuf<pb::RecOut> d_rec_;
     DevBuf<double> d_dig_, d_del_, d_bpv_;
     DevBuf<int> d_bpk_;
@@ -407,6 +408,7 @@ void Batch::build() {
     d_rid_.ensure(rq);
     d_rs_.ensure(rq);
     d_aoff32_.ensure(rq);
+    d_blocked_.ensure(rq);
     d_rec_.ensure(rq);
     d_cand_.ensure(rq);
     d_tmp_.ensure(rq);
@@ -484,6 +486,7 @@ pb::Arena Batch::arena(bool oracle) const {
     a.spec = d_spec_.p;
     a.aoff = d_aoff_.p;
     a.aoff32 = d_aoff32_.p;
+    a.blocked = d_blocked_.p;
     a.rs = d_rs_.p;
     a.rec = d_rec_.p;
     a.ph = d_ph_.p;
@@ -616,10 +619,10 @@ void Batch::fetch_single(RunOutputs& o, bool records, bool log) {
         }
         o.aoff.resize(n);
         down(o.aoff.data(), d_aoff_.p, n * sizeof(long long));
-        std::vector<pb::PacerHot> ph(n);
-        down(ph.data(), d_ph_.p, n * sizeof(pb::PacerHot));
+        std::vector<pb::ReqState> rs(n);
+        down(rs.data(), d_rs_.p, n * sizeof(pb::ReqState));
         // the delivered count travels in rec.pad for the dump writer
-        for (long long k = 0; k < n; ++k) o.rec[k].pad = ph[k].ndel;
+        for (long long k = 0; k < n; ++k) o.rec[k].pad = rs[k].ndel;
     }
     if (log) {
         pb::ReplicaOut ro;

@@ -51,10 +51,10 @@ __global__ void rows_kernel(const int* rid, const MetricParams* params, const in
     double ttfat = __dsub_rn(r.first_answer_delivery, r.reasoning_end);
     // qoe (metrics.cpp:38-52)
     double q = 1.0;
-    const PacerHot p = ph[g];
-    int nd = p.ndel;
+    int nd = rs[g].ndel;
     long long n = sp.z;
     if (n >= 1 && nd > 0) {
+        const PacerHot p = ph[g];
         const double* bv = bpv + aoff[g];
         const int* bk = bpk + aoff[g];
         double t0 = r.first_answer_delivery;
