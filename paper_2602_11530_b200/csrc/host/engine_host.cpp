@@ -83,6 +83,8 @@ public:
 
 private:
     static size_t round(size_t b) {
+        static const int mode = std::getenv("PB_POOL_ROUND") ? std::atoi(std::getenv("PB_POOL_ROUND")) : 1;
+        if (mode == 0) return std::max<size_t>(b, 1);
         const size_t q = b >= (64u << 20) ? (2u << 20) : (b >= (1u << 20) ? (64u << 10) : 512);
         return (std::max<size_t>(b, 1) + q - 1) / q * q;
     }
