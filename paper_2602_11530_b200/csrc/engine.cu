@@ -1747,7 +1747,11 @@ __global__ void __launch_bounds__(128, MINB) sched_kernel(Arena a, int max_ni, i
     char* smem = smem_raw + (size_t)warp * smem_per_warp(max_ni, n_smem, c_smem, h_slots);
     while (true) {
         int r = 0;
-        if (lane_id() == 0) r = atomicAdd(a.work, 1);
+        if (lane_id() == 0) {
+            r = atomicAdd(a.work, 1);
+            if (r < a.n_rep) r = a.order[r];
+            else r = a.n_rep;
+        }
         r = __shfl_sync(FULL, r, 0);
         if (r >= a.n_rep) break;
         run_replica(a, r, smem, max_ni, n_smem, c_smem, h_slots);

@@ -133,6 +133,7 @@ struct Arena {
     ReplicaOut* out;
     int n_rep;
     int* work;  // work-stealing counter
+    const int* order;  // replicas in hand-out order (longest predicted first)
     // read-only trace
     const double* arrival;
     const int4* spec;       // {prompt, reasoning, answering, kv_preloaded}

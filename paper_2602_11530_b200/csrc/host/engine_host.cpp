@@ -243,14 +243,14 @@ public:
               total_log_ = 0;
     std::vector<pb::ReplicaDesc> desc_;
     std::vector<pb::ReplicaDesc> odesc_;  // oracle pre-run descriptors
-    std::vector<int> omap_;
+    std::vector<int> omap_, order_, oorder_;
     std::vector<long long> echo_static_;
 
     cudaStream_t st_ = nullptr;
     cudaEvent_t ev_[5] = {};
     DevBuf<pb::ReplicaDesc> d_desc_, d_odesc_, d_desc_init_;
     DevBuf<pb::ReplicaOut> d_out_, d_oout_;
-    DevBuf<int> d_work_, d_omap_, d_rid_;
+    DevBuf<int> d_work_, d_omap_, d_rid_, d_order_, d_oorder_;
     DevBuf<double> d_arrival_, d_frac_;
     DevBuf<int4> d_spec_, d_cand_, d_tmp_;
     DevBuf<pb::ReqState> d_rs_;
@@ -460,6 +460,28 @@ void Batch::build() {
     up(d_desc_init_.p, desc_.data(), desc_.size() * sizeof(pb::ReplicaDesc));
     up(d_odesc_.p, odesc_.data(), odesc_.size() * sizeof(pb::ReplicaDesc));
     up(d_omap_.p, omap_.data(), omap_.size() * sizeof(int));
+    // Longest-predicted-first hand-out order for the work-stealing loop (the
+    // step ends with its slowest warp): cost ~ request-iterations, doubled
+    // for the queue-scanning policies.
+    {
+        auto cost = [&](int r) {
+            double c = (double)request_iterations(*jobs_[r].trace);
+            return jobs_[r].cfg.policy == pb::kPascal || jobs_[r].cfg.policy == pb::kRr ? 2 * c : c;
+        };
+        std::vector<double> cr(n_rep_);
+        for (int r = 0; r < n_rep_; ++r) cr[r] = cost(r);
+        order_.resize(n_rep_);
+        std::iota(order_.begin(), order_.end(), 0);
+        std::stable_sort(order_.begin(), order_.end(), [&](int a, int b) { return cr[a] > cr[b]; });
+        oorder_.resize(odesc_.size());
+        std::iota(oorder_.begin(), oorder_.end(), 0);
+        std::stable_sort(oorder_.begin(), oorder_.end(),
+                         [&](int a, int b) { return cr[omap_[a]] > cr[omap_[b]]; });
+        d_order_.ensure(n_rep_);
+        d_oorder_.ensure(oorder_.size());
+        up(d_order_.p, order_.data(), order_.size() * sizeof(int));
+        up(d_oorder_.p, oorder_.data(), oorder_.size() * sizeof(int));
+    }
     up(d_arrival_.p, arrival.data(), arrival.size() * sizeof(double));
     up(d_spec_.p, spec.data(), spec.size() * sizeof(int4));
     up(d_aoff_.p, aoff.data(), aoff.size() * sizeof(long long));
@@ -484,6 +506,7 @@ pb::Arena Batch::arena(bool oracle) const {
     a.out = oracle ? d_oout_.p : d_out_.p;
     a.n_rep = oracle ? (int)odesc_.size() : n_rep_;
     a.work = d_work_.p + (oracle ? 0 : 1);
+    a.order = oracle ? d_oorder_.p : d_order_.p;
     a.arrival = d_arrival_.p;
     a.spec = d_spec_.p;
     a.aoff = d_aoff_.p;
