@@ -224,11 +224,12 @@ constexpr int kHistBins = 128;  // PASCAL_HIST_BINS
 int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots,
                   int warps_per_block, int blocks, void* stream);
 // capacity = max(ceil(fraction * peak / ni), biggest) for the replicas listed
-// in `map` (derive_capacity, proj/src/engine.cpp:466-470); writes echo[r] and,
-// unless the replica runs the oracle policy, desc[r].capacity.
+// in `map`, peak from oracle pre-run oref[k] (derive_capacity,
+// proj/src/engine.cpp:466-470); writes echo[r] and, unless the replica runs
+// the oracle policy, desc[r].capacity.
 int launch_capacity(ReplicaDesc* desc, const ReplicaOut* oracle_out, const int* map,
-                    const double* fraction, const long long* biggest, long long* echo,
-                    int count, void* stream);
+                    const int* oref, const double* fraction, const long long* biggest,
+                    long long* echo, int count, void* stream);
 int launch_histograms(const int* rid, const int* group, const RowArrays rows,
                       const ReplicaOut* out, long long total, int n_groups,
                       unsigned long long* hist, unsigned long long* slo, void* stream);

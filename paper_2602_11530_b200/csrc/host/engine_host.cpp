@@ -18,6 +18,7 @@
 #include <memory>
 #include <mutex>
 #include <numeric>
+#include <string>
 #include <unordered_map>
 
 #include "common.hpp"
@@ -243,14 +244,14 @@ public:
               total_log_ = 0;
     std::vector<pb::ReplicaDesc> desc_;
     std::vector<pb::ReplicaDesc> odesc_;  // oracle pre-run descriptors
-    std::vector<int> omap_, order_, oorder_;
+    std::vector<int> omap_, oref_, orep_, order_, oorder_;  // omap_/oref_: replica -> its pre-run
     std::vector<long long> echo_static_;
 
     cudaStream_t st_ = nullptr;
     cudaEvent_t ev_[5] = {};
     DevBuf<pb::ReplicaDesc> d_desc_, d_odesc_, d_desc_init_;
     DevBuf<pb::ReplicaOut> d_out_, d_oout_;
-    DevBuf<int> d_work_, d_omap_, d_rid_, d_order_, d_oorder_;
+    DevBuf<int> d_work_, d_omap_, d_oref_, d_rid_, d_order_, d_oorder_;
     DevBuf<double> d_arrival_, d_frac_;
     DevBuf<int4> d_spec_, d_cand_, d_tmp_;
     DevBuf<pb::ReqState> d_rs_;
@@ -310,6 +311,9 @@ void Batch::build() {
     echo_static_.assign(n_rep_, 0);
     odesc_.clear();
     omap_.clear();
+    oref_.clear();
+    orep_.clear();
+    std::map<std::string, int> oracle_of;
     long long rq = 0, ans = 0, q = 0, bt = 0, hp = 0, lg = 0;
     for (int r = 0; r < n_rep_; ++r) {
         const Job& j = jobs_[r];
@@ -345,13 +349,37 @@ void Batch::build() {
             d.capacity = j.cfg.policy == pb::kOracle ? kOracleCap : echo_static_[r];
         } else {
             d.capacity = kOracleCap;  // overwritten by the capacity kernel unless oracle
-            pb::ReplicaDesc od = d;
-            od.policy = pb::kOracle;
-            od.flags = 0;
-            od.capacity = kOracleCap;
-            od.log_cap = 0;
-            odesc_.push_back(od);
+            // One oracle pre-run per distinct (trace, instances, profile, ...):
+            // the oracle never evicts, demotes, paces or counts quanta, so the
+            // peak it measures does not depend on the policy, the ablations
+            // or the capacity fraction (a sweep over those shares one).
+            std::string key(reinterpret_cast<const char*>(&j.trace), sizeof(j.trace));
+            auto add = [&key](const void* p, size_t b) {
+                key.append(reinterpret_cast<const char*>(p), b);
+            };
+            add(&ni, sizeof ni);
+            add(&j.prof, sizeof j.prof);
+            add(&d.quantum, sizeof d.quantum);
+            add(&d.demotion, sizeof d.demotion);
+            add(&d.slack, sizeof d.slack);
+            add(&d.tpot, sizeof d.tpot);
+            auto it = oracle_of.find(key);
+            int k;
+            if (it != oracle_of.end()) {
+                k = it->second;
+            } else {
+                pb::ReplicaDesc od = d;
+                od.policy = pb::kOracle;
+                od.flags = 0;
+                od.capacity = kOracleCap;
+                od.log_cap = 0;
+                k = (int)odesc_.size();
+                odesc_.push_back(od);
+                orep_.push_back(r);
+                oracle_of.emplace(std::move(key), k);
+            }
             omap_.push_back(r);
+            oref_.push_back(k);
         }
         desc_[r] = d;
         params[r] = pb::MetricParams{j.cfg.tpot, j.cfg.qoe_threshold, j.cfg.ttfat_target, rq,
@@ -403,6 +431,7 @@ void Batch::build() {
     d_odesc_.ensure(odesc_.size());
     d_oout_.ensure(odesc_.size());
     d_omap_.ensure(omap_.size());
+    d_oref_.ensure(oref_.size());
     d_work_.ensure(2);
     d_arrival_.ensure(rq);
     d_spec_.ensure(rq);
@@ -460,6 +489,7 @@ void Batch::build() {
     up(d_desc_init_.p, desc_.data(), desc_.size() * sizeof(pb::ReplicaDesc));
     up(d_odesc_.p, odesc_.data(), odesc_.size() * sizeof(pb::ReplicaDesc));
     up(d_omap_.p, omap_.data(), omap_.size() * sizeof(int));
+    up(d_oref_.p, oref_.data(), oref_.size() * sizeof(int));
     // Longest-predicted-first hand-out order for the work-stealing loop (the
     // step ends with its slowest warp): cost ~ request-iterations, doubled
     // for the queue-scanning policies.
@@ -476,7 +506,7 @@ void Batch::build() {
         oorder_.resize(odesc_.size());
         std::iota(oorder_.begin(), oorder_.end(), 0);
         std::stable_sort(oorder_.begin(), oorder_.end(),
-                         [&](int a, int b) { return cr[omap_[a]] > cr[omap_[b]]; });
+                         [&](int a, int b) { return cr[orep_[a]] > cr[orep_[b]]; });
         d_order_.ensure(n_rep_);
         d_oorder_.ensure(oorder_.size());
         up(d_order_.p, order_.data(), order_.size() * sizeof(int));
@@ -550,8 +580,8 @@ void Batch::execute() {
         pb::Arena oa = arena(true);
         if (launch(oa, (int)odesc_.size(), max_on_))
             throw std::logic_error("engine launch failed (oracle pre-run)");
-        if (pb::launch_capacity(d_desc_.p, d_oout_.p, d_omap_.p, d_frac_.p, d_biggest_.p,
-                                d_echo_.p, (int)odesc_.size(), st_))
+        if (pb::launch_capacity(d_desc_.p, d_oout_.p, d_omap_.p, d_oref_.p, d_frac_.p,
+                                d_biggest_.p, d_echo_.p, (int)omap_.size(), st_))
             throw std::logic_error("capacity kernel launch failed");
         launches += 2;
     }

@@ -24,13 +24,13 @@ namespace pb {
 constexpr unsigned FULLM = 0xffffffffu;
 
 __global__ void capacity_kernel(ReplicaDesc* desc, const ReplicaOut* oout, const int* map,
-                                const double* fraction, const long long* biggest,
-                                long long* echo, int count) {
+                                const int* oref, const double* fraction,
+                                const long long* biggest, long long* echo, int count) {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= count) return;
-    int r = map[k];
+    int r = map[k];  // replica, and the oracle pre-run it shares
     double f = fraction[r] > 0.0 ? fraction[r] : 1.0;
-    double q = __ddiv_rn(__dmul_rn(f, (double)oout[k].peak), (double)desc[r].ni);
+    double q = __ddiv_rn(__dmul_rn(f, (double)oout[oref[k]].peak), (double)desc[r].ni);
     long long cap = (long long)ceil(q);
     if (cap < biggest[r]) cap = biggest[r];
     echo[r] = cap;
@@ -206,11 +206,11 @@ int launch_histograms(const int* rid, const int* group, const RowArrays rows,
 }
 
 int launch_capacity(ReplicaDesc* desc, const ReplicaOut* oracle_out, const int* map,
-                    const double* fraction, const long long* biggest, long long* echo,
-                    int count, void* stream) {
+                    const int* oref, const double* fraction, const long long* biggest,
+                    long long* echo, int count, void* stream) {
     if (count <= 0) return 0;
     capacity_kernel<<<(count + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
-        desc, oracle_out, map, fraction, biggest, echo, count);
+        desc, oracle_out, map, oref, fraction, biggest, echo, count);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
