@@ -5,7 +5,7 @@
 //   arrival placement   engine.cpp:260-283, cluster.cpp:10-33,59-62
 //   monitor snapshot    instance.cpp:22-33,59-76, engine.cpp:103-109
 //   demotion            instance.cpp:39-57
-//   planner             instance.cpp:103-282               -> plan_and_apply()
+//   planner             instance.cpp:103-282               -> maybe_start()
 //   plan application    engine.cpp:192-258
 //   iteration retire    engine.cpp:310-337, instance.cpp:10-20
 //   phase boundary      engine.cpp:159-190, cluster.cpp:35-57,64-68
@@ -157,7 +157,7 @@ struct Rep {
     // request arrays (offset to this replica)
     const double* arrival;
     int4* spec;
-    int* aoff;  // answer-slot offset relative to dig / del
+    int* aoff;  // answer-slot offset relative to the replica's bpv / bpk / dig / del
     ReqState* rs;
     double* blocked;
     RecOut* rec;
