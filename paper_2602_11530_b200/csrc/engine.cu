@@ -1542,7 +1542,7 @@ DEVI int on_transfer_complete(Rep& R, Scal& S, int idx) {
 
 // ------------------------------------------------------------ the replica
 DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem, int c_smem,
-                      int h_slots) {
+                      int h_slots, int b_smem) {
     const ReplicaDesc d = a.desc[r];
     Rep R;
     R.n = d.n;
@@ -1614,6 +1614,9 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     R.s_tmp = R.s_cand + c_smem;
     R.s_tmpq = reinterpret_cast<unsigned*>(R.s_tmp + c_smem);
     R.s_cstat = reinterpret_cast<unsigned char*>(R.s_tmpq + c_smem);
+    sp += smem_cand_bytes(c_smem);
+    const bool blocked_smem = !resident && R.n <= b_smem;
+    if (blocked_smem) R.blocked = reinterpret_cast<double*>(sp);
     for (int i = lane_id(); i < ni; i += 32) {
         R.s.gpu[i] = 0;
         R.s.cpu[i] = 0;
@@ -1741,10 +1744,10 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
 // MINB = 4: throughput shape (16 warps per SM, <= 128 registers per thread).
 template <int MINB>
 __global__ void __launch_bounds__(128, MINB) sched_kernel(Arena a, int max_ni, int n_smem, int c_smem,
-                                                          int h_slots) {
+                                                          int h_slots, int b_smem) {
     extern __shared__ __align__(16) char smem_raw[];
     const int warp = threadIdx.x >> 5;
-    char* smem = smem_raw + (size_t)warp * smem_per_warp(max_ni, n_smem, c_smem, h_slots);
+    char* smem = smem_raw + (size_t)warp * smem_per_warp(max_ni, n_smem, c_smem, h_slots, b_smem);
     while (true) {
         int r = 0;
         if (lane_id() == 0) {
@@ -1754,14 +1757,15 @@ __global__ void __launch_bounds__(128, MINB) sched_kernel(Arena a, int max_ni, i
         }
         r = __shfl_sync(FULL, r, 0);
         if (r >= a.n_rep) break;
-        run_replica(a, r, smem, max_ni, n_smem, c_smem, h_slots);
+        run_replica(a, r, smem, max_ni, n_smem, c_smem, h_slots, b_smem);
     }
 }
 
-int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots,
+int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
                   int warps_per_block, int blocks, void* stream) {
     if (warps_per_block < 1 || warps_per_block > 4 || h_slots < 2) return 1;
-    const size_t smem = (size_t)warps_per_block * smem_per_warp(max_ni, n_smem, c_smem, h_slots);
+    const size_t smem =
+        (size_t)warps_per_block * smem_per_warp(max_ni, n_smem, c_smem, h_slots, b_smem);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1777,7 +1781,7 @@ int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slot
     if (const char* cv = getenv("PB_CARVEOUT"))  // experiment hook: shared-memory carveout %
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
     kern<<<blocks, warps_per_block * 32, smem, (cudaStream_t)stream>>>(a, max_ni, n_smem, c_smem,
-                                                                       h_slots);
+                                                                       h_slots, b_smem);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

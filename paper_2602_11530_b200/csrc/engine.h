@@ -213,15 +213,20 @@ PB_HD inline int smem_heap_bytes(int n_smem, int ni, int h_slots = kSmemHeapSlot
     return n_smem ? (n_smem + ni + 2) * 16 : h_slots * 16;
 }
 PB_HD inline int smem_cand_bytes(int c_smem) { return (c_smem * 37 + 15) / 16 * 16; }
-PB_HD inline int smem_per_warp(int ni, int n_smem, int c_smem, int h_slots = kSmemHeapSlots) {
+// HBM-resident replicas with n <= b_smem keep their blocked-time totals (the
+// most frequently written per-request value: one read-modify-write per denial)
+// in shared memory.
+PB_HD inline int smem_blocked_bytes(int b_smem) { return (b_smem * 8 + 15) / 16 * 16; }
+PB_HD inline int smem_per_warp(int ni, int n_smem, int c_smem, int h_slots = kSmemHeapSlots,
+                               int b_smem = 0) {
     return smem_inst_bytes(ni) + smem_req_bytes(n_smem) + smem_heap_bytes(n_smem, ni, h_slots) +
-           smem_cand_bytes(c_smem);
+           smem_cand_bytes(c_smem) + smem_blocked_bytes(b_smem);
 }
 
 constexpr int kHistBins = 128;  // PASCAL_HIST_BINS
 
 // Host entries (engine.cu / metrics.cu). All enqueue on `stream`.
-int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots,
+int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
                   int warps_per_block, int blocks, void* stream);
 // capacity = max(ceil(fraction * peak / ni), biggest) for the replicas listed
 // in `map`, peak from oracle pre-run oref[k] (derive_capacity,

@@ -129,7 +129,7 @@ struct DevBuf {
 // replicas -> one warp per CTA so they spread over all SMs; many -> up to four
 // per CTA, as many as the shared-memory budget allows.
 struct Shape {
-    int n_smem, c_smem, wpb, blocks, h_slots;
+    int n_smem, c_smem, wpb, blocks, h_slots, b_smem;
 };
 
 Shape pick_shape(int reps, int max_ni, int max_n) {
@@ -155,15 +155,27 @@ Shape pick_shape(int reps, int max_ni, int max_n) {
         return std::max(0, std::min(kMaxWarpsPerSm, sm_budget / std::max(1, per_warp)));
     };
     // A: request state + heap + candidate scratch in shared memory
-    Shape a{max_n, std::min(max_n, 1024), 0, 0, h_slots};
+    Shape a{max_n, std::min(max_n, 1024), 0, 0, h_slots, 0};
     int pa = pb::smem_per_warp(max_ni, a.n_smem, a.c_smem, h_slots);
     bool a_ok = pa <= budget && mode != 0;
     // B: request state in HBM (L2-resident), small shared candidate scratch
     const char* cenv = std::getenv("PB_CAND_SMEM");  // experiment hook: scratch slots
-    Shape b{0, std::min(max_n, cenv ? std::max(32, std::atoi(cenv)) : 512), 0, 0, h_slots};
-    while (b.c_smem > 32 && pb::smem_per_warp(max_ni, 0, b.c_smem, h_slots) * 8 > sm_budget)
+    Shape b{0, std::min(max_n, cenv ? std::max(32, std::atoi(cenv)) : 512), 0, 0, h_slots, 0};
+    // blocked-time totals in shared memory when they fit beside a candidate
+    // scratch of >= 256 slots at 8 warps per SM (C2: 2,000 requests = 16 KB)
+    const char* benv = std::getenv("PB_BLOCKED_SMEM");  // experiment hook: 0 disables
+    if (!benv || std::atoi(benv) != 0) {
+        Shape t = b;
+        t.b_smem = max_n;
+        while (t.c_smem > 256 &&
+               pb::smem_per_warp(max_ni, 0, t.c_smem, h_slots, t.b_smem) * 8 > sm_budget)
+            t.c_smem /= 2;
+        if (pb::smem_per_warp(max_ni, 0, t.c_smem, h_slots, t.b_smem) * 8 <= sm_budget) b = t;
+    }
+    while (b.c_smem > 32 &&
+           pb::smem_per_warp(max_ni, 0, b.c_smem, h_slots, b.b_smem) * 8 > sm_budget)
         b.c_smem /= 2;
-    int pbw = pb::smem_per_warp(max_ni, 0, b.c_smem, h_slots);
+    int pbw = pb::smem_per_warp(max_ni, 0, b.c_smem, h_slots, b.b_smem);
     const bool use_a = a_ok && (mode == 1 || warps_fit(pa) >= std::min(need_w, 4));
     Shape sh = use_a ? a : b;
     const int per_warp = use_a ? pa : pbw;
@@ -567,8 +579,8 @@ void Batch::execute() {
     Timing& tm = g_timing;
     auto launch = [&](const pb::Arena& ar, int reps, int max_n) {
         const Shape sh = pick_shape(reps, max_ni_, max_n);
-        return pb::launch_engine(ar, max_ni_, sh.n_smem, sh.c_smem, sh.h_slots, sh.wpb, sh.blocks,
-                                 st_);
+        return pb::launch_engine(ar, max_ni_, sh.n_smem, sh.c_smem, sh.h_slots, sh.b_smem, sh.wpb,
+                                 sh.blocks, st_);
     };
     int launches = 0;
     ck(cudaEventRecord(ev_[0], st_), "event");
