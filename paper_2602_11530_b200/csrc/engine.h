@@ -226,8 +226,17 @@ PB_HD inline int smem_per_warp(int ni, int n_smem, int c_smem, int h_slots = kSm
 constexpr int kHistBins = 128;  // PASCAL_HIST_BINS
 
 // Host entries (engine.cu / metrics.cu). All enqueue on `stream`.
+// Two builds of the engine: `logging` writes the pascal-events-v1 decision
+// log (kLogEvents) and the full delivery / digest arrays (kRecordDeliv);
+// `nolog` has every log and record site compiled out.
+namespace logging {
 int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
                   int warps_per_block, int blocks, void* stream);
+}
+namespace nolog {
+int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
+                  int warps_per_block, int blocks, void* stream);
+}
 // capacity = max(ceil(fraction * peak / ni), biggest) for the replicas listed
 // in `map`, peak from oracle pre-run oref[k] (derive_capacity,
 // proj/src/engine.cpp:466-470); writes echo[r] and, unless the replica runs

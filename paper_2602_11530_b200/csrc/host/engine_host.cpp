@@ -579,8 +579,10 @@ void Batch::execute() {
     Timing& tm = g_timing;
     auto launch = [&](const pb::Arena& ar, int reps, int max_n) {
         const Shape sh = pick_shape(reps, max_ni_, max_n);
-        return pb::launch_engine(ar, max_ni_, sh.n_smem, sh.c_smem, sh.h_slots, sh.b_smem, sh.wpb,
-                                 sh.blocks, st_);
+        auto eng = log_cap_ > 0 || records_ ? pb::logging::launch_engine
+                                            : pb::nolog::launch_engine;
+        return eng(ar, max_ni_, sh.n_smem, sh.c_smem, sh.h_slots, sh.b_smem, sh.wpb, sh.blocks,
+                   st_);
     };
     int launches = 0;
     ck(cudaEventRecord(ev_[0], st_), "event");
