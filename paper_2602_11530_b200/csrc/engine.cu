@@ -1575,7 +1575,11 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     Rep R;
     R.n = d.n;
     R.ni = d.ni;
+#ifdef PB_ONLY_POLICY
+    R.policy = PB_ONLY_POLICY;  // single-policy build: every policy test folds
+#else
     R.policy = d.policy;
+#endif
     R.flags = d.flags;
     R.cap = d.capacity;
     R.quantum = d.quantum;

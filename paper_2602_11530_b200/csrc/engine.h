@@ -237,6 +237,16 @@ namespace nolog {
 int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
                   int warps_per_block, int blocks, void* stream);
 }
+// `nolog` specialised to replicas that all run the Pascal policy, and to the
+// Oracle policy of the capacity pre-run.
+namespace pascal_lean {
+int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
+                  int warps_per_block, int blocks, void* stream);
+}
+namespace oracle_lean {
+int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
+                  int warps_per_block, int blocks, void* stream);
+}
 // capacity = max(ceil(fraction * peak / ni), biggest) for the replicas listed
 // in `map`, peak from oracle pre-run oref[k] (derive_capacity,
 // proj/src/engine.cpp:466-470); writes echo[r] and, unless the replica runs

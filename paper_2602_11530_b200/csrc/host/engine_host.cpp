@@ -577,10 +577,19 @@ pb::Arena Batch::arena(bool oracle) const {
 void Batch::execute() {
     build();
     Timing& tm = g_timing;
-    auto launch = [&](const pb::Arena& ar, int reps, int max_n) {
+    const char* penv = std::getenv("PB_NO_POLICY_SPECIALISATION");  // experiment hook
+    const bool all_pascal =
+        !(penv && std::atoi(penv)) &&
+        std::all_of(desc_.begin(), desc_.end(),
+                    [](const pb::ReplicaDesc& d) { return d.policy == pb::kPascal; });
+    auto launch = [&](const pb::Arena& ar, int reps, int max_n, int variant) {
         const Shape sh = pick_shape(reps, max_ni_, max_n);
-        auto eng = log_cap_ > 0 || records_ ? pb::logging::launch_engine
-                                            : pb::nolog::launch_engine;
+        // 0: the policy run, generic; 1: the policy run, all Pascal; 2: the
+        // oracle pre-run (never logs or records)
+        auto eng = variant == 2                      ? pb::oracle_lean::launch_engine
+                   : (log_cap_ > 0 || records_)      ? pb::logging::launch_engine
+                   : variant == 1                    ? pb::pascal_lean::launch_engine
+                                                     : pb::nolog::launch_engine;
         return eng(ar, max_ni_, sh.n_smem, sh.c_smem, sh.h_slots, sh.b_smem, sh.wpb, sh.blocks,
                    st_);
     };
@@ -592,7 +601,7 @@ void Batch::execute() {
     ck(cudaMemsetAsync(d_work_.p, 0, 2 * sizeof(int), st_), "memset");
     if (!odesc_.empty()) {
         pb::Arena oa = arena(true);
-        if (launch(oa, (int)odesc_.size(), max_on_))
+        if (launch(oa, (int)odesc_.size(), max_on_, penv && std::atoi(penv) ? 0 : 2))
             throw std::logic_error("engine launch failed (oracle pre-run)");
         if (pb::launch_capacity(d_desc_.p, d_oout_.p, d_omap_.p, d_oref_.p, d_frac_.p,
                                 d_biggest_.p, d_echo_.p, (int)omap_.size(), st_))
@@ -601,7 +610,7 @@ void Batch::execute() {
     }
     ck(cudaEventRecord(ev_[1], st_), "event");
     pb::Arena pa = arena(false);
-    if (launch(pa, n_rep_, max_n_))
+    if (launch(pa, n_rep_, max_n_, all_pascal ? 1 : 0))
         throw std::logic_error("engine launch failed");
     launches += 1;
     ck(cudaEventRecord(ev_[2], st_), "event");
