@@ -237,13 +237,21 @@ namespace nolog {
 int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
                   int warps_per_block, int blocks, void* stream);
 }
-// `nolog` specialised to replicas that all run the Pascal policy, and to the
-// Oracle policy of the capacity pre-run.
+// `nolog` specialised to batches whose replicas all run one policy (Pascal,
+// Oracle — also the capacity pre-run —, FCFS, RR).
 namespace pascal_lean {
 int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
                   int warps_per_block, int blocks, void* stream);
 }
 namespace oracle_lean {
+int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
+                  int warps_per_block, int blocks, void* stream);
+}
+namespace fcfs_lean {
+int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
+                  int warps_per_block, int blocks, void* stream);
+}
+namespace rr_lean {
 int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
                   int warps_per_block, int blocks, void* stream);
 }

@@ -578,18 +578,29 @@ void Batch::execute() {
     build();
     Timing& tm = g_timing;
     const char* penv = std::getenv("PB_NO_POLICY_SPECIALISATION");  // experiment hook
-    const bool all_pascal =
-        !(penv && std::atoi(penv)) &&
-        std::all_of(desc_.begin(), desc_.end(),
-                    [](const pb::ReplicaDesc& d) { return d.policy == pb::kPascal; });
-    auto launch = [&](const pb::Arena& ar, int reps, int max_n, int variant) {
+    const bool spec = !(penv && std::atoi(penv));
+    // the policy all replicas share (-1: mixed)
+    int common = desc_.empty() ? -1 : desc_[0].policy;
+    for (const pb::ReplicaDesc& d : desc_)
+        if (d.policy != common) common = -1;
+    using Launcher = int (*)(const pb::Arena&, int, int, int, int, int, int, int, void*);
+    auto lean_for = [](int policy) -> Launcher {
+        switch (policy) {
+            case pb::kPascal: return pb::pascal_lean::launch_engine;
+            case pb::kOracle: return pb::oracle_lean::launch_engine;
+            case pb::kFcfs: return pb::fcfs_lean::launch_engine;
+            case pb::kRr: return pb::rr_lean::launch_engine;
+            default: return pb::nolog::launch_engine;
+        }
+    };
+    // `pre_run`: the oracle capacity pre-run (never logs or records)
+    auto launch = [&](const pb::Arena& ar, int reps, int max_n, bool pre_run) {
         const Shape sh = pick_shape(reps, max_ni_, max_n);
-        // 0: the policy run, generic; 1: the policy run, all Pascal; 2: the
-        // oracle pre-run (never logs or records)
-        auto eng = variant == 2                      ? pb::oracle_lean::launch_engine
-                   : (log_cap_ > 0 || records_)      ? pb::logging::launch_engine
-                   : variant == 1                    ? pb::pascal_lean::launch_engine
-                                                     : pb::nolog::launch_engine;
+        Launcher eng = pre_run                        ? (spec ? lean_for(pb::kOracle)
+                                                              : pb::nolog::launch_engine)
+                       : (log_cap_ > 0 || records_)   ? pb::logging::launch_engine
+                       : spec                          ? lean_for(common)
+                                                       : pb::nolog::launch_engine;
         return eng(ar, max_ni_, sh.n_smem, sh.c_smem, sh.h_slots, sh.b_smem, sh.wpb, sh.blocks,
                    st_);
     };
@@ -601,7 +612,7 @@ void Batch::execute() {
     ck(cudaMemsetAsync(d_work_.p, 0, 2 * sizeof(int), st_), "memset");
     if (!odesc_.empty()) {
         pb::Arena oa = arena(true);
-        if (launch(oa, (int)odesc_.size(), max_on_, penv && std::atoi(penv) ? 0 : 2))
+        if (launch(oa, (int)odesc_.size(), max_on_, true))
             throw std::logic_error("engine launch failed (oracle pre-run)");
         if (pb::launch_capacity(d_desc_.p, d_oout_.p, d_omap_.p, d_oref_.p, d_frac_.p,
                                 d_biggest_.p, d_echo_.p, (int)omap_.size(), st_))
@@ -610,7 +621,7 @@ void Batch::execute() {
     }
     ck(cudaEventRecord(ev_[1], st_), "event");
     pb::Arena pa = arena(false);
-    if (launch(pa, n_rep_, max_n_, all_pascal ? 1 : 0))
+    if (launch(pa, n_rep_, max_n_, false))
         throw std::logic_error("engine launch failed");
     launches += 1;
     ck(cudaEventRecord(ev_[2], st_), "event");
