@@ -1783,13 +1783,12 @@ __global__ void __launch_bounds__(128, MINB) sched_kernel(Arena a, int max_ni, i
     char* smem = smem_raw + (size_t)warp * smem_per_warp(max_ni, n_smem, c_smem, h_slots, b_smem);
     while (true) {
         int r = 0;
-        if (lane_id() == 0) {
-            r = atomicAdd(a.work, 1);
-            if (r < a.n_rep) r = a.order[r];
-            else r = a.n_rep;
+        if (lane_id() == 0) {  // a.order lists this launch's replicas (maybe a subset)
+            const int w = atomicAdd(a.work, 1);
+            r = w < a.n_rep ? a.order[w] : -1;
         }
         r = __shfl_sync(FULL, r, 0);
-        if (r >= a.n_rep) break;
+        if (r < 0) break;
         run_replica<TAIL_FAST>(a, r, smem, max_ni, n_smem, c_smem, h_slots, b_smem);
     }
 }
