@@ -17,7 +17,10 @@ end of each step; timing is the max over ranks of the device step time.
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/ref_dump = /root/reference/proj compiled unmodified; falls back to
-the oracle port) on the same workload with all host cores.
+the oracle port) on the same workload with all host cores. That arm never
+imports this repo's package: its traces come from the reference generator
+(`ref_dump gen` / `mix`), and its replicas are a seed prefix of the GPU arm's
+(seeds 1..S), run as one longest-first pool of >= 4 replicas per core.
 """
 from __future__ import annotations
 
@@ -36,7 +39,20 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-from paper_2602_11530_b200 import sweep  # noqa: E402
+
+def _load_sweep():
+    """paper_2602_11530_b200/sweep.py as a standalone module: replica recipes
+    are pure Python, and the reference arm must not import the package (nor
+    load libpascal.so)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_bench_sweep", os.path.join(ROOT, "paper_2602_11530_b200", "sweep.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+sweep = _load_sweep()
 
 METRIC = "scheduled request-iterations/sec (1/2/4/8 B200) + P99 TTFT/SLO match vs CPU ref"
 UNIT = "request-iterations/s"
@@ -172,75 +188,122 @@ def find_cpu_ref():
     return port, "port"
 
 
-def cpu_time_replicas(specs, procs, tmp, outputs=None):
-    """Run the CPU reference on `specs` with `procs` parallel processes; returns
-    (wall seconds, request-iterations). With `outputs` (a list), each replica's
-    (ttft_p99, slo_violation_rate, ttft_mean) from the reference is appended."""
-    import paper_2602_11530_b200 as pb
-    from cases import cfg_text
-    from harness import build_trace
+def ref_trace_hex(exe, recipe, out, tmp):
+    """Materialise a trace recipe with the REFERENCE generator (ref_dump gen /
+    mix: proj/src/workload.cpp), never through libpascal.so."""
+    if "gen" in recipe:
+        n, rate, pd, rd, ad, seed, pre = recipe["gen"]
+        subprocess.run([exe, "gen", str(n), repr(float(rate)), pd, rd, ad, str(seed),
+                        str(int(pre)), out], check=True)
+        return
+    base, repl, frac, seed = recipe["mix"]
+    a, b = out + ".a", out + ".b"
+    ref_trace_hex(exe, base, a, tmp)
+    ref_trace_hex(exe, repl, b, tmp)
+    subprocess.run([exe, "mix", a, b, repr(float(frac)), str(seed), out], check=True)
 
-    exe, _ = find_cpu_ref()
-    jobs = []
-    units = 0
+
+def hex_request_iterations(path):
+    """SURVEY.md §8d closed form over a pascal-trace-hex-v1 file:
+    T = sum(R + A - [R = 0 and not preloaded] + [not preloaded])."""
+    t = 0
+    with open(path) as f:
+        next(f)
+        for line in f:
+            _, _, _, r, a, pre = line.split()
+            r, a, pre = int(r), int(a), int(pre)
+            t += r + a - (1 if (r == 0 and not pre) else 0) + (0 if pre else 1)
+    return t
+
+
+def cfg_text(cfg, prof):
+    import math
+    lines = [f"{k}={v}" for k, v in cfg.items()]
+    for k, v in prof.items():
+        lines.append(f"{k}={'inf' if math.isinf(float(v)) else repr(float(v))}")
+    return "\n".join(lines) + "\n"
+
+
+def cpu_time_replicas(specs, procs, tmp, outputs=None):
+    """Run the CPU reference (`ref_dump sim` = engine::run incl. its capacity
+    pre-run) on `specs` with `procs` concurrent processes, handed out
+    longest-first from one pool (no step waits on a straggler while cores
+    idle); returns (wall seconds, request-iterations). With `outputs` (a
+    list), each replica's (ttft_p99, slo_violation_rate, ttft_mean) from the
+    reference is appended in spec order."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    exe, kind = find_cpu_ref()
+    jobs, units, cost = [], 0, []
     for i, (recipe, cfg, prof) in enumerate(specs):
-        t = build_trace(recipe)
-        units += t.request_iterations()
         hexp = os.path.join(tmp, f"r{i}.hex")
-        t.save_hex(hexp)
+        if kind == "reference":
+            ref_trace_hex(exe, recipe, hexp, tmp)
+        else:  # the C port has no generator: fall back to the product's (checker-side only)
+            from harness import build_trace
+            build_trace(recipe).save_hex(hexp)
+        u = hex_request_iterations(hexp)
+        units += u
+        cost.append(u * (1 if cfg.get("policy") == "fcfs" else 2))
         cfgp = os.path.join(tmp, f"r{i}.cfg")
         with open(cfgp, "w") as f:
-            f.write(cfg_text({"cfg": cfg, "profile": prof}))
+            f.write(cfg_text(cfg, prof))
         jobs.append([exe, "sim", hexp, cfgp])
+    order = sorted(range(len(jobs)), key=lambda i: -cost[i])
+    res = [None] * len(jobs)
+
+    def one(i):
+        r = subprocess.run(jobs[i], capture_output=True, text=True, check=True)
+        res[i] = r.stdout
+
     t0 = time.perf_counter()
-    running = []
-    done = []
-    for j in jobs:
-        while len(running) >= procs:
-            done.append(running.pop(0))
-            done[-1].wait()
-        running.append(subprocess.Popen(j, stdout=subprocess.PIPE, text=True))
-    for p in running:
-        p.wait()
-        done.append(p)
+    with ThreadPoolExecutor(max(1, procs)) as ex:
+        list(ex.map(one, order))
     dt = time.perf_counter() - t0
     if outputs is not None:
-        for p in done:
-            f = p.stdout.read().split()
+        for out in res:
+            f = out.split()
             outputs.append(tuple(float.fromhex(x) for x in f[1:4]))
     return dt, units
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's own CPU scheduler on all host cores."""
-    cores = os.cpu_count() or 1
+    """--impl reference: the reference's own CPU scheduler on all host cores.
+    Rank 0 alone runs (the CPU arm does not shard over GPUs); other ranks exit."""
     if rank != 0:
         return
+    cores = os.cpu_count() or 1
     exe, kind = find_cpu_ref()
     desc, _ = WORKLOADS[args.workload]
-    # bounded sample per step: one replica per host core (whole replicas, never truncated)
-    per_step = args.ref_replicas or cores
-    specs = replica_specs(args.workload, 0, per_step)
+    # Bounded sample: a seed prefix (1..S) of the GPU arm's replicas, S = 4
+    # replicas per host core (>= one per step), run as ONE longest-first pool
+    # over all K steps so no step ends waiting on a straggler; the per-step
+    # figure is the pool's wall time / K. (One C2 replica is ~10 s on a core,
+    # so the whole arm takes ~40 s on 16 cores whatever K is.)
+    total = args.ref_replicas or max(4 * cores, args.steps)
+    specs = replica_specs(args.workload, 0, total)
     with tempfile.TemporaryDirectory() as tmp:
         for _ in range(args.warmup):  # warm-up: a single small replica (page-in, caches)
             cpu_time_replicas(replica_specs("c1", 0, 1), 1, tmp)
-        times, units = [], 0
-        for _ in range(args.steps):
-            dt, u = cpu_time_replicas(specs, cores, tmp)
-            times.append(dt)
-            units = u
-    tot = sum(times)
-    value = units * args.steps / tot
+        wall, units = cpu_time_replicas(specs, cores, tmp)
+    value = units / wall
+    seeds = "seeds 1..%d" % total if args.workload != "c5" else "C5 replica ids %d..%d" % (
+        C5_IDS[0], C5_IDS[total - 1])
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * wall / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generator, seeds 1..)",
-        "config": {"workload": desc, "replicas_per_step": per_step,
-                   "timed": "engine::run incl. capacity pre-run, one process per replica"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(cores, per_step),
-                         "kind": kind, "sample": f"{per_step} whole {args.workload} replicas "
-                                                 f"per step, {cores} host cores"},
+        "data": "synthetic (reference trace generator ref_dump gen/mix, same recipes as the "
+                "B200 arm)",
+        "config": {"workload": desc, "replicas_total": total, "sample": seeds,
+                   "request_iterations_total": units,
+                   "timed": "engine::run incl. capacity pre-run, one process per replica, "
+                            f"{cores} concurrent, longest-first"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(cores, total),
+                         "kind": kind,
+                         "sample": f"{total} whole {args.workload} replicas ({seeds}, a prefix "
+                                   f"of the B200 arm's), one longest-first pool on {cores} host "
+                                   f"cores; ms_per_step = pool wall / steps"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -299,11 +362,14 @@ def main():
     def gather(summ):
         """End-of-step exchange: NCCL all-gather of per-replica summaries and
         all-reduce of the device TTFT histograms / SLO counters."""
+        h, sl = batch.histograms()
+        return gather_from(summ, h, sl)
+
+    def gather_from(summ, h, sl):
         rows = torch.tensor([[float(base_id + k), s.ttft_mean, s.ttft_p50, s.ttft_p99,
                               s.slo_violation_rate, s.throughput, float(s.requests),
                               float(s.request_iterations), float(s.status)]
                              for k, s in enumerate(summ)], dtype=torch.float64)
-        h, sl = batch.histograms()
         h = torch.tensor(h, dtype=torch.int64)
         sl = torch.tensor(sl, dtype=torch.int64)
         if world > 1:
@@ -316,14 +382,24 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # A step = simulate (oracle pre-run + policy run + metrics, on the engine's
+    # stream; execute() returns when it is done) + the end-of-step exchange
+    # (NCCL all-gather / all-reduce on torch's stream at N > 1). The step is
+    # bracketed by CUDA events on torch's stream, recorded before the launch
+    # and after the collective, so the collective is inside the timed region.
     step_ms, engine_ms, launches = [], [], 0
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
+            ev0.record()
             batch.execute()
             tm = pb.last_timing()
             summ = batch.summaries()
             grows, ghist, gslo = gather(summ)
-            step_ms.append(tm.total_ms)
+            ev1.record()
+            ev1.synchronize()
+            step_ms.append(ev0.elapsed_time(ev1))
             engine_ms.append(tm.engine_ms)
             launches += tm.kernel_launches
     torch.cuda.synchronize()
@@ -346,15 +422,29 @@ def main():
     value = tot_units / (ms_step / 1000.0)
     del batch
 
-    # ---- e2e through the public C-ABI call with host buffers (H2D + D2H inside)
+    # ---- e2e through the public API with host buffers: trace upload (H2D),
+    # simulation, summaries + histograms back (D2H) and, at N > 1, the NCCL
+    # exchange, every step
     e2e_times = []
+    h2d = d2h = 0
     for i in range(max(1, min(args.steps, 3))):
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        summ2 = pb.run_batch(traces, profs, cfgs)
-        e2e_times.append(time.perf_counter() - t0)
+        b2 = pb.Batch(traces, profs, cfgs)
+        tm_up = pb.last_timing()
+        b2.set_groups(groups, ngroups)
+        b2.execute()
+        summ2 = b2.summaries()
         tm2 = pb.last_timing()
+        h2, s2 = b2.histograms()
+        ex_rows, _, _ = gather_from(summ2, h2, s2)
+        if world > 1:
+            torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+        h2d = int(tm_up.h2d_bytes)
+        d2h = int(tm2.d2h_bytes) + 8 * ngroups * (len(h2[0]) + 2)
+        del b2
     e2e_s = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64)
     if world > 1:
         e2e_d = e2e_s.to(dev)
@@ -404,11 +494,15 @@ def main():
         "data": "synthetic (reference trace generator, seeds 1..)",
         "config": {"workload": desc, "replicas_per_gpu": per_gpu,
                    "request_iterations_per_step": tot_units,
-                   "timed": "oracle capacity pre-run + policy run + metrics, all on device",
+                   "timed": "oracle capacity pre-run + policy run + metrics on device + "
+                            "end-of-step summary/histogram exchange (NCCL at N > 1), CUDA "
+                            "events on torch's stream around the whole step",
                    "l2": "inputs larger than L2 (per-replica arenas > 126 MB total)",
                    "parallelism": f"replica shards x{world}"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(tm2.h2d_bytes),
-                "d2h_bytes_per_step": int(tm2.d2h_bytes)},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "timed": "pb.Batch(host traces) upload + execute + summaries/histograms "
+                         "download" + (" + NCCL exchange" if world > 1 else "")},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,

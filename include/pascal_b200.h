@@ -120,6 +120,11 @@ pascal_status pascal_trace_get(const pascal_trace* t, long i, long* id, double* 
  * [not preloaded]). */
 long long pascal_trace_request_iterations(const pascal_trace* t);
 
+/* Releases every idle device block the library's caching allocator holds
+ * (on every device). Blocks in use by live batches are not affected. The
+ * idle cache is also bounded by PB_POOL_CACHE_MB (default 16384) per device. */
+pascal_status pascal_release_cached_memory(void);
+
 /* One process per GPU: selects the CUDA device for this thread. */
 pascal_status pascal_set_device(int device);
 /* 1 when a usable CUDA device is present (no kernels are launched). */

@@ -9,7 +9,15 @@ and stores sha256/line counts (plus full text for tiny cases) under
 tests/golden/. The GPU tests recompute the same artefacts through
 libpascal.so and compare.
 
-    python oracle/make_golden.py [--only NAME ...] [--skip-large]
+    python oracle/make_golden.py [--only NAME ...] [--skip-large] [--jobs J]
+                                 [--sizes xlarge huge ...] [--missing]
+
+Sizes "xlarge" / "huge" / "thrash" (tests/cases.py) go through
+`ref_dump all`: one capacity derivation + one simulation with that capacity
+made explicit (identical results, see oracle/ref_dump.cpp) + the report files
+with pascal_run's config echo, instead of the three simulations of the
+run + capacity + C-ABI path. "huge" (C4 at 1M requests) pipes its records
+straight into sha256sum (~26 GB of text is never stored).
 """
 from __future__ import annotations
 
@@ -21,6 +29,8 @@ import os
 import subprocess
 import sys
 import tempfile
+import time
+from concurrent.futures import ProcessPoolExecutor, as_completed
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -109,22 +119,100 @@ def ref_config(lib, c):
     return cfg, prof
 
 
+BIG = ("xlarge", "huge", "thrash")
+
+
+def golden_big(c, timeout):
+    """One `ref_dump all` run (records sha, reports; no decision log)."""
+    name = c["name"]
+    with tempfile.TemporaryDirectory(dir="/tmp") as tmp:
+        trace = os.path.join(tmp, name + ".hex")
+        build_trace_hex(c["trace"], trace, tmp)
+        cfgp = os.path.join(tmp, name + ".cfg")
+        with open(cfgp, "w") as f:
+            f.write(cfg_text(c))
+        prefix = os.path.join(tmp, name + ".rep")
+        rec = os.path.join(tmp, name + ".rec")
+        rec_spec = f"|sha256sum > {rec}.sha" if c["size"] == "huge" else rec
+        t0 = time.time()
+        try:
+            r = subprocess.run([REF_DUMP, "all", trace, cfgp, rec_spec, "-", prefix],
+                               check=True, capture_output=True, text=True, timeout=timeout)
+        except subprocess.TimeoutExpired:
+            return name, {"timeout_s": timeout}
+        info = json.loads(r.stdout)
+        if c["size"] == "huge":
+            records = [open(rec + ".sha").read().split()[0], c_requests(trace)]
+        else:
+            records = list(sha_file(rec))
+        g = {"trace": list(sha_file(trace)), "records": records, "events": None,
+             "capacity": info["capacity"], "ref_derive_s": info["derive_s"],
+             "ref_run_s": info["run_s"], "ref_wall_s": round(time.time() - t0, 1),
+             "report": {ext: list(sha_file(prefix + "." + ext))
+                        for ext in ("requests.csv", "summary.txt", "bins.csv")}}
+        with open(prefix + ".summary.txt") as f:
+            g["summary_text"] = f.read()
+        return name, g
+
+
+def c_requests(trace_hex):
+    with open(trace_hex) as f:
+        return sum(1 for _ in f) - 1
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*")
     ap.add_argument("--skip-large", action="store_true")
+    ap.add_argument("--sizes", nargs="*", help="only cases of these sizes")
+    ap.add_argument("--missing", action="store_true", help="only cases not in the index")
+    ap.add_argument("--jobs", type=int, default=1, help="parallel workers (xlarge/huge/thrash)")
     ap.add_argument("--timeout", type=float, default=300.0)
     args = ap.parse_args()
     os.makedirs(GOLD, exist_ok=True)
     lib = _lib.bind(C.CDLL(REF_SO), extensions=False)
     index_path = os.path.join(GOLD, "index.json")
     index = json.load(open(index_path)) if os.path.exists(index_path) else {}
+
+    mine = {}
+
+    def save():
+        # several generator processes may run at once: merge under a lock
+        import fcntl
+        with open(index_path + ".lock", "w") as lk:
+            fcntl.flock(lk, fcntl.LOCK_EX)
+            cur = json.load(open(index_path)) if os.path.exists(index_path) else {}
+            cur.update(mine)
+            with open(index_path + ".tmp", "w") as f:
+                json.dump(cur, f, indent=1, sort_keys=True)
+            os.replace(index_path + ".tmp", index_path)
+
+    def wanted(c):
+        if args.only and c["name"] not in args.only:
+            return False
+        if args.skip_large and c["size"] == "large":
+            return False
+        if args.sizes and c["size"] not in args.sizes:
+            return False
+        if args.missing and c["name"] in index and "timeout_s" not in index[c["name"]]:
+            return False
+        return True
+
+    big = [c for c in CASES if wanted(c) and c["size"] in BIG]
+    if big:
+        with ProcessPoolExecutor(max(1, args.jobs)) as ex:
+            futs = [ex.submit(golden_big, c, None if c["size"] == "huge" else args.timeout)
+                    for c in big]
+            for fu in as_completed(futs):
+                name, g = fu.result()
+                index[name] = mine[name] = g
+                print(f"{name:28s} {json.dumps({k: g.get(k) for k in ('capacity', 'ref_run_s', 'timeout_s')})}",
+                      flush=True)
+                save()
     with tempfile.TemporaryDirectory() as tmp:
         for c in CASES:
             name = c["name"]
-            if args.only and name not in args.only:
-                continue
-            if args.skip_large and c["size"] == "large":
+            if not wanted(c) or c["size"] in BIG:
                 continue
             trace = os.path.join(tmp, name + ".hex")
             build_trace_hex(c["trace"], trace, tmp)
@@ -160,12 +248,11 @@ def main():
                 with open(prefix + ".summary.txt") as f, \
                         open(os.path.join(GOLD, f"{name}.summary.txt"), "w") as o:
                     o.write(f.read())
-            index[name] = g
+            index[name] = mine[name] = g
             print(f"{name:28s} records={g['records'][1]:6d} "
                   f"events={g['events'][1] if g['events'] else '-':>9} "
                   f"cap={g['capacity']}", flush=True)
-            with open(index_path, "w") as f:
-                json.dump(index, f, indent=1, sort_keys=True)
+            save()
 
 
 if __name__ == "__main__":

@@ -10,6 +10,14 @@
 //   ref_dump report TRACE.hex CFG PREFIX           (build_report + write_report)
 //   ref_dump sim  TRACE.hex CFG                    (engine::run only, no output files;
 //                                                   the bench.py reference arm)
+//   ref_dump all  TRACE.hex CFG RECORDS|-|'|cmd' EVENTS|-|'|cmd' PREFIX
+//        one derive_capacity + one engine::run with that capacity made explicit
+//        (identical by engine.cpp:370-377,456: derive_capacity(explicit c) =
+//        max(c, biggest) = c), records / event log (a leading '|' pipes into a
+//        shell command, e.g. '|sha256sum > x'), and the three pascal-report-v1
+//        files with the config echo pascal_run writes (proj/src/capi.cpp:
+//        189-203). Prints {"capacity", "derive_s", "run_s"}. For the large
+//        goldens, where the C-ABI path would simulate twice more.
 //
 // Trace files use the lossless hex-float format "pascal-trace-hex-v1"
 // (one line per request: id arrival(%a) prompt reasoning answering preloaded).
@@ -76,6 +84,7 @@ void write_hex_trace(const workload::Trace& t, const std::string& path) {
 struct Cfg {
     engine::RunConfig rc;
     costmodel::LatencyProfile prof;
+    std::string policy = "pascal";
 };
 
 Cfg read_cfg(const std::string& path) {
@@ -94,7 +103,7 @@ Cfg read_cfg(const std::string& path) {
         else if (k == "capacity_fraction") c.rc.capacity_fraction = d;
         else if (k == "token_quantum") c.rc.token_quantum = l;
         else if (k == "demotion_threshold") c.rc.demotion_threshold = l;
-        else if (k == "policy") c.rc.policy = engine::parse_policy(v);
+        else if (k == "policy") c.rc.policy = engine::parse_policy(v), c.policy = v;
         else if (k == "no_migration") c.rc.ablations.no_migration = l != 0;
         else if (k == "non_adaptive") c.rc.ablations.non_adaptive = l != 0;
         else if (k == "target_tpot") c.rc.target_tpot = d;
@@ -120,6 +129,31 @@ void dump_records(const std::vector<metrics::RequestRecord>& recs, FILE* f) {
         std::fprintf(f, "\n");
     }
 }
+
+// Output sink: a file, or a shell pipeline when the spec starts with '|'.
+struct Sink {
+    FILE* f = nullptr;
+    bool pipe = false;
+    explicit Sink(const std::string& spec) {
+        if (spec == "-") return;
+        pipe = !spec.empty() && spec[0] == '|';
+        f = pipe ? popen(spec.c_str() + 1, "w") : std::fopen(spec.c_str(), "w");
+        if (!f) throw std::runtime_error("cannot open " + spec);
+    }
+    ~Sink() {
+        if (f) pipe ? pclose(f) : std::fclose(f);
+    }
+};
+
+// std::ostream over a FILE* (the event log writer takes an ostream).
+struct FileBuf : std::streambuf {
+    FILE* f;
+    explicit FileBuf(FILE* fp) : f(fp) {}
+    int overflow(int c) override { return c == EOF ? 0 : std::fputc(c, f); }
+    std::streamsize xsputn(const char* s, std::streamsize n) override {
+        return (std::streamsize)std::fwrite(s, 1, (size_t)n, f);
+    }
+};
 
 int usage() {
     std::fprintf(stderr, "usage: see header of oracle/ref_dump.cpp\n");
@@ -191,6 +225,41 @@ int main(int argc, char** argv) {
                                              c.rc.ttfat_target);
             std::printf("%zu %a %a %a\n", recs.size(), rep.ttft_p99, rep.slo_violation_rate,
                         rep.ttft_mean);
+        } else if (mode == "all" && argc == 7) {
+            using clk = std::chrono::steady_clock;
+            auto t = read_hex_trace(argv[2]);
+            Cfg c = read_cfg(argv[3]);
+            auto t0 = clk::now();
+            const long cap = engine::derive_capacity(t, c.rc, c.prof);
+            auto t1 = clk::now();
+            engine::RunConfig rc = c.rc;
+            rc.gpu_capacity = cap;
+            Sink ev(argv[5]);
+            FileBuf eb(ev.f);
+            std::ostream evs(&eb);
+            auto recs = engine::run(t, rc, c.prof, ev.f ? &evs : nullptr);
+            evs.flush();
+            auto t2 = clk::now();
+            {
+                Sink rs(argv[4]);
+                if (rs.f) dump_records(recs, rs.f);
+            }
+            auto rep = metrics::build_report(recs, c.rc.target_tpot, c.rc.qoe_threshold,
+                                             c.rc.ttfat_target);
+            rep.config_echo = {
+                {"policy", c.policy},
+                {"instance_count", std::to_string(c.rc.instance_count)},
+                {"gpu_capacity", std::to_string(cap)},
+                {"token_quantum", std::to_string(c.rc.token_quantum)},
+                {"demotion_threshold", std::to_string(c.rc.demotion_threshold)},
+                {"no_migration", std::to_string(c.rc.ablations.no_migration)},
+                {"non_adaptive", std::to_string(c.rc.ablations.non_adaptive)},
+                {"requests", std::to_string(t.size())},
+            };
+            metrics::write_report(rep, argv[6]);
+            std::printf("{\"capacity\": %ld, \"derive_s\": %.3f, \"run_s\": %.3f}\n", cap,
+                        std::chrono::duration<double>(t1 - t0).count(),
+                        std::chrono::duration<double>(t2 - t1).count());
         } else if (mode == "report" && argc == 5) {
             auto t = read_hex_trace(argv[2]);
             Cfg c = read_cfg(argv[3]);

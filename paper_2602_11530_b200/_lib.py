@@ -27,7 +27,8 @@ ABI_SYMBOLS = (
     "pascal_run_batch", "pascal_last_timing", "pascal_run_dump", "pascal_derive_capacity",
     "pascal_trace_load_hex", "pascal_trace_save_hex", "pascal_trace_from_arrays",
     "pascal_trace_get", "pascal_trace_request_iterations", "pascal_set_device",
-    "pascal_device_available", "pascal_batch_set_groups", "pascal_batch_histograms",
+    "pascal_device_available", "pascal_release_cached_memory", "pascal_batch_set_groups",
+    "pascal_batch_histograms",
     "pascal_sweep",
 )
 HIST_BINS = 128
@@ -146,6 +147,7 @@ def bind(lib: C.CDLL, extensions: bool = True) -> C.CDLL:
         "pascal_trace_request_iterations": (C.c_longlong, [P]),
         "pascal_set_device": (st, [C.c_int]),
         "pascal_device_available": (C.c_int, []),
+        "pascal_release_cached_memory": (st, []),
         "pascal_batch_set_groups": (st, [P, C.POINTER(C.c_int), C.c_int]),
         "pascal_batch_histograms": (st, [P, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
         "pascal_sweep": (st, [P, P, C.POINTER(RunConfig), C.POINTER(C.c_char_p), C.c_size_t,

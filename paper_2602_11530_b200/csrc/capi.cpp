@@ -572,4 +572,8 @@ pascal_status pascal_set_device(int device) {
 
 int pascal_device_available(void) { return device_available() ? 1 : 0; }
 
+pascal_status pascal_release_cached_memory(void) {
+    return guarded([&] { release_cached_memory(); });
+}
+
 }  // extern "C"

@@ -166,6 +166,7 @@ struct Timing {
     int launches = 0;
 };
 Timing& last_timing();
+void release_cached_memory();
 void set_device(int dev);
 bool device_available();
 

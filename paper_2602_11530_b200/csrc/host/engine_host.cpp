@@ -34,11 +34,31 @@ void ck(cudaError_t e, const char* what) {
         throw std::logic_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 
+// Switches the calling thread to `dev` for a scope and restores the
+// previous device after it.
+struct ScopedDevice {
+    int prev = -1;
+    explicit ScopedDevice(int dev) {
+        if (dev < 0) return;
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~ScopedDevice() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 // Device allocations are cached per device for the life of the process: a
 // batch of thousands of replicas allocates ~20 arenas of up to GBs, and
 // cudaMalloc / cudaFree of those cost 0.3-1 s per end-to-end call against a
 // ~5.7 s simulation. Freed blocks are reused for requests of up to 2x smaller
 // size; on an out-of-memory the cache is released and the allocation retried.
+// Every block remembers the device it was allocated on and returns to that
+// device's free list whatever device is current when it is released. The
+// cache is bounded (PB_POOL_CACHE_MB, default 16 GiB per device of idle
+// blocks; the largest idle blocks are released first) and can be released
+// explicitly (pascal_release_cached_memory).
 class DevicePool {
 public:
     void* get(size_t bytes) {
@@ -51,7 +71,8 @@ public:
             auto it = fl.lower_bound(bytes);
             if (it != fl.end() && it->first <= 2 * bytes) {
                 void* p = it->second;
-                sizes_[p] = it->first;
+                live_[p] = Block{it->first, dev};
+                idle_bytes_[dev] -= it->first;
                 fl.erase(it);
                 return p;
             }
@@ -63,26 +84,56 @@ public:
             ck(cudaMalloc(&p, bytes), "cudaMalloc");
         }
         std::lock_guard<std::mutex> g(m_);
-        sizes_[p] = bytes;
+        live_[p] = Block{bytes, dev};
         return p;
     }
     void put(void* p) {
         if (!p) return;
-        int dev = 0;
-        cudaGetDevice(&dev);
         std::lock_guard<std::mutex> g(m_);
-        auto it = sizes_.find(p);
-        if (it == sizes_.end()) return;
-        free_[dev].emplace(it->second, p);
-        sizes_.erase(it);
+        auto it = live_.find(p);
+        if (it == live_.end()) return;
+        const Block b = it->second;
+        live_.erase(it);
+        free_[b.dev].emplace(b.bytes, p);
+        idle_bytes_[b.dev] += b.bytes;
+        // bound the idle cache: release the largest idle blocks first
+        auto& fl = free_[b.dev];
+        while (idle_bytes_[b.dev] > cap_bytes() && !fl.empty()) {
+            auto last = std::prev(fl.end());
+            ScopedDevice sd(b.dev);
+            cudaFree(last->second);
+            idle_bytes_[b.dev] -= last->first;
+            fl.erase(last);
+        }
     }
     void trim(int dev) {
         std::lock_guard<std::mutex> g(m_);
-        for (auto& kv : free_[dev]) cudaFree(kv.second);
-        free_[dev].clear();
+        trim_locked(dev);
+    }
+    void trim_all() {
+        std::lock_guard<std::mutex> g(m_);
+        for (auto& kv : free_) trim_locked(kv.first);
     }
 
 private:
+    struct Block {
+        size_t bytes;
+        int dev;
+    };
+    void trim_locked(int dev) {
+        ScopedDevice sd(dev);
+        for (auto& kv : free_[dev]) cudaFree(kv.second);
+        free_[dev].clear();
+        idle_bytes_[dev] = 0;
+    }
+    static size_t cap_bytes() {
+        static const size_t cap = [] {
+            const char* e = std::getenv("PB_POOL_CACHE_MB");
+            const long long mb = e ? std::atoll(e) : 16384;
+            return (size_t)std::max<long long>(0, mb) << 20;
+        }();
+        return cap;
+    }
     static size_t round(size_t b) {
         static const int mode = std::getenv("PB_POOL_ROUND") ? std::atoi(std::getenv("PB_POOL_ROUND")) : 1;
         if (mode == 0) return std::max<size_t>(b, 1);
@@ -96,7 +147,8 @@ private:
     }
     std::mutex m_;
     std::map<int, std::multimap<size_t, void*>> free_;
-    std::unordered_map<void*, size_t> sizes_;
+    std::map<int, size_t> idle_bytes_;
+    std::unordered_map<void*, Block> live_;
 };
 
 DevicePool& pool() {
@@ -215,6 +267,8 @@ void check_limits(const Job& j) {
 
 Timing& last_timing() { return g_timing; }
 
+void release_cached_memory() { pool().trim_all(); }
+
 bool device_available() {
     int n = 0;
     return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
@@ -250,6 +304,7 @@ public:
     bool records_ = false;
     long long log_cap_ = 0;
     bool built_ = false;
+    int dev_ = -1;  // the device the batch's arenas and stream live on
 
     int n_rep_ = 0, max_ni_ = 1, max_n_ = 0, max_on_ = 0;
     long long total_req_ = 0, total_ans_ = 0, total_q_ = 0, total_batch_ = 0, total_heap_ = 0,
@@ -301,6 +356,7 @@ Batch::Batch(const std::vector<Job>& jobs) : jobs_(jobs) {
 }
 
 Batch::~Batch() {
+    ScopedDevice sd(dev_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     if (st_) cudaStreamDestroy(st_);
@@ -309,6 +365,7 @@ Batch::~Batch() {
 void Batch::build() {
     if (built_) return;
     built_ = true;
+    ck(cudaGetDevice(&dev_), "cudaGetDevice");
     n_rep_ = (int)jobs_.size();
     ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
     for (auto& e : ev_) ck(cudaEventCreate(&e), "event");
@@ -576,6 +633,7 @@ pb::Arena Batch::arena(bool oracle) const {
 
 void Batch::execute() {
     build();
+    ScopedDevice sd(dev_);
     Timing& tm = g_timing;
     const char* penv = std::getenv("PB_NO_POLICY_SPECIALISATION");  // experiment hook
     const bool spec = !(penv && std::atoi(penv));
@@ -653,6 +711,7 @@ void Batch::execute() {
 }
 
 void Batch::fetch_summaries(std::vector<DeviceSummary>& out) {
+    ScopedDevice sd(dev_);
     static_assert(sizeof(DeviceSummary) == sizeof(pb::DevSummary), "summary layout");
     out.resize(n_rep_);
     ck(cudaEventRecord(ev_[0], st_), "event");
@@ -668,6 +727,7 @@ void Batch::fetch_summaries(std::vector<DeviceSummary>& out) {
 }
 
 void Batch::fetch_single(RunOutputs& o, bool records, bool log) {
+    ScopedDevice sd(dev_);
     std::vector<DeviceSummary> s;
     fetch_summaries(s);
     o.summary = s[0];
@@ -725,6 +785,7 @@ void Batch::fetch_single(RunOutputs& o, bool records, bool log) {
 
 // Per-request metric rows of every replica (trace order within a replica).
 void Batch::fetch_rows(std::vector<std::vector<Row>>& rows) {
+    ScopedDevice sd(dev_);
     const long long n = total_req_;
     std::vector<double> ttft(n), ttfat(n), qoe(n), blk(n);
     std::vector<unsigned char> slo(n);
@@ -773,6 +834,7 @@ void batch_free(Batch* b) { delete b; }
 
 void batch_set_groups(Batch* b, const int* group_of_replica, int n_groups) {
     if (n_groups < 1) throw std::invalid_argument("n_groups must be >= 1");
+    ScopedDevice sd(b->dev_);
     for (int r = 0; r < b->n_rep_; ++r)
         if (group_of_replica[r] < 0 || group_of_replica[r] >= n_groups)
             throw std::invalid_argument("group id out of range");
@@ -787,6 +849,7 @@ void batch_set_groups(Batch* b, const int* group_of_replica, int n_groups) {
 
 void batch_histograms(Batch* b, unsigned long long* hist, unsigned long long* slo) {
     if (b->n_groups_ == 0) throw std::invalid_argument("no groups set on this batch");
+    ScopedDevice sd(b->dev_);
     ck(cudaMemcpy(hist, b->d_hist_.p,
                   sizeof(unsigned long long) * b->n_groups_ * (pb::kHistBins + 2),
                   cudaMemcpyDeviceToHost),

@@ -168,4 +168,34 @@ CASES.append(case("c4s_pascal", cli_mixed(20000, 16.0, 1), "pascal", size="xlarg
 CASES.append(case("c4s_fcfs", cli_mixed(20000, 16.0, 1), "fcfs", size="xlarge",
                   instance_count=64, capacity_fraction=0.9))
 
+# C3 across the arrival-rate sweep (BASELINE.json configs[2]: lambda in
+# {2, 4, 8, 16}) for all four policy variants, plus the
+# stress point lambda = 8 at capacity 0.5 where the reference is O(Q^2).
+C3_VARIANTS = (("pascal", "pascal", {}), ("nomig", "pascal", {"no_migration": 1}),
+               ("nonadaptive", "pascal", {"non_adaptive": 1}), ("fcfs", "fcfs", {}))
+_have = {c["name"] for c in CASES}
+for lam in (2, 4, 8, 16):
+    for name, pol, extra in C3_VARIANTS:
+        if f"c3_l{lam}_{name}" in _have:
+            continue
+        CASES.append(case(f"c3_l{lam}_{name}", gen(20000, float(lam), CHAT, 1), pol,
+                          size="xlarge", instance_count=8, capacity_fraction=0.9, **extra))
+for name, pol, extra in C3_VARIANTS:
+    CASES.append(case(f"c3x_l8_{name}", gen(20000, 8.0, CHAT, 1), pol, size="xlarge",
+                      instance_count=8, capacity_fraction=0.5, **extra))
+# C4 at its stated size (BASELINE.json configs[3]: CLI mixed preset,
+# pascalsim_cli.cpp:174-193, 1M requests, 64 instances, lambda 16, cap 0.9):
+# records sha (piped, never stored) + report files.
+for name, pol in (("pascal", "pascal"), ("fcfs", "fcfs")):
+    CASES.append(case(f"c4_full_{name}", cli_mixed(1000000, 16.0, 1), pol, size="huge",
+                      instance_count=64, capacity_fraction=0.9))
+# C5 rates k = 0..2 (lambda = 1, 1.26, 1.59 req/s) at capacity 0.5: the
+# evict / swap-in thrash regime (BASELINE.json configs[4]).
+for s in (0, 1):
+    for k in (0, 1, 2):
+        rate = 2.0 ** (k / 3.0)
+        for name, pol, extra in C3_VARIANTS:
+            CASES.append(case(f"c5_s{s}_k{k}_{name}", acc_mixed(256, rate, s), pol, ACC,
+                              size="thrash", instance_count=4, capacity_fraction=0.5, **extra))
+
 BY_NAME = {c["name"]: c for c in CASES}
