@@ -43,7 +43,8 @@ typedef struct {
     double h2d_ms, d2h_ms;
     long long h2d_bytes, d2h_bytes;
     int kernel_launches;
-    int pad;
+    int instance_parallel; /* policy-run replicas completed by the instance-parallel engine
+                              (the rest ran on the warp-per-replica engine) */
 } pascal_timing;
 
 typedef struct pascal_batch pascal_batch;

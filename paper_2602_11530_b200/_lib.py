@@ -78,7 +78,7 @@ class Timing(C.Structure):
         ("derive_ms", C.c_double), ("engine_ms", C.c_double), ("metrics_ms", C.c_double),
         ("total_ms", C.c_double), ("h2d_ms", C.c_double), ("d2h_ms", C.c_double),
         ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong),
-        ("kernel_launches", C.c_int), ("pad", C.c_int),
+        ("kernel_launches", C.c_int), ("instance_parallel", C.c_int),
     ]
 
 

@@ -461,7 +461,7 @@ pascal_status pascal_last_timing(pascal_timing* out) {
         out->h2d_bytes = t.h2d_bytes;
         out->d2h_bytes = t.d2h_bytes;
         out->kernel_launches = t.launches;
-        out->pad = 0;
+        out->instance_parallel = t.instance_parallel;
     });
 }
 

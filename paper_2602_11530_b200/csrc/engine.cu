@@ -27,6 +27,7 @@
 // in descending order (a stack), restricted to the class-eligible suffix.
 
 #include <cuda_runtime.h>
+#include <math_constants.h>
 
 #include <cfloat>
 #include <climits>
@@ -44,6 +45,16 @@
 #define PB_LOG 1
 #define PB_VARIANT logging
 #endif
+// PB_PDES = 1 builds the instance-parallel engine (pdes_kernel below) instead
+// of the warp-per-replica one: one CTA per replica, instance i owned by warp
+// i % W, instances advance concurrently between cross-instance interactions
+// (arrivals, Pascal phase boundaries). Never combined with the decision log.
+#ifndef PB_PDES
+#define PB_PDES 0
+#endif
+#if PB_PDES && PB_LOG
+#error "the instance-parallel engine has no decision-log build"
+#endif
 
 namespace pb {
 namespace PB_VARIANT {
@@ -59,13 +70,26 @@ DEVI unsigned m_loc(unsigned m) { return (m >> 2) & 3u; }
 DEVI bool m_swin(unsigned m) { return (m >> 4) & 1u; }
 DEVI bool m_swout(unsigned m) { return (m >> 5) & 1u; }
 DEVI bool m_qlow(unsigned m) { return (m >> 6) & 1u; }
-DEVI int m_owner(unsigned m) { return (int)(m >> 8); }
+// PDES builds keep the owner in bits 8..23 and, in bits 24..31, min(255,
+// tokens left until the request's phase boundary) (engine_pdes.cuh horizon).
+DEVI int m_owner(unsigned m) { return PB_PDES ? (int)((m >> 8) & 0xffffu) : (int)(m >> 8); }
 DEVI unsigned m_set_phase(unsigned m, unsigned p) { return (m & ~3u) | p; }
+// PDES builds: rem = tokens until the phase boundary (a decode iteration
+// holding a reasoning request with rem == 1 is a cross-instance event under
+// Pascal); meaningful in the waiting / reasoning phases only.
+DEVI unsigned m_rem(unsigned m) { return m >> 24; }
+DEVI unsigned m_set_rem(unsigned m, long long r) {
+    const unsigned v = r < 0 ? 0u : (r > 255 ? 255u : (unsigned)r);
+    return (m & 0x00ffffffu) | (v << 24);
+}
+DEVI bool m_tnext(unsigned m) { return ((m & 3u) == 1u) && m_rem(m) == 1u; }  // PH_REASON
 DEVI unsigned m_set_loc(unsigned m, unsigned l) { return (m & ~(3u << 2)) | (l << 2); }
 DEVI unsigned m_set_swin(unsigned m, bool b) { return (m & ~(1u << 4)) | ((unsigned)b << 4); }
 DEVI unsigned m_set_swout(unsigned m, bool b) { return (m & ~(1u << 5)) | ((unsigned)b << 5); }
 DEVI unsigned m_set_qlow(unsigned m, bool b) { return (m & ~(1u << 6)) | ((unsigned)b << 6); }
-DEVI unsigned m_set_owner(unsigned m, int o) { return (m & 0xffu) | ((unsigned)o << 8); }
+DEVI unsigned m_set_owner(unsigned m, int o) {
+    return PB_PDES ? (m & 0xff0000ffu) | ((unsigned)o << 8) : (m & 0xffu) | ((unsigned)o << 8);
+}
 // instance.hpp:59-61
 DEVI bool m_resident(unsigned m) { return m_loc(m) == LOC_GPU && !m_swin(m) && !m_swout(m); }
 // instance.cpp:86-90 (a queued request is never Done)
@@ -74,7 +98,7 @@ DEVI bool m_candidate(unsigned m) {
 }
 
 // candidate flags (int4::w of the candidate scratch)
-constexpr int CF_LOW = 1, CF_WAIT = 2, CF_RES = 4, CF_QPOS = 8;
+constexpr int CF_LOW = 1, CF_WAIT = 2, CF_RES = 4, CF_QPOS = 8, CF_TNEXT = 16;
 // candidate status
 constexpr unsigned char CS_ADMIT = 1, CS_DENY = 2;
 
@@ -157,6 +181,16 @@ struct Inst {  // shared-memory SoA for the replica's instances
     int* blen;
     int* busy;
     int* healthy;
+#if PB_PDES
+    // per-instance event heaps and sequence counters (instance-parallel engine)
+    int* hn;                    // heap entries
+    int* hspill;                // heap moved to its HBM region
+    unsigned* enq;              // enqueue-seq counter (seqs are (k * ni + i))
+    unsigned long long* evseq;  // event-seq counter (tie-break within the instance's heap)
+    double* gtime;              // time of the pending cross-instance event, else +inf
+    int* dmin;                  // min rem (tokens to a phase boundary) over the queued
+                                // waiting / reasoning requests, as of the last plan
+#endif
 };
 
 struct Rep {
@@ -199,6 +233,12 @@ struct Rep {
     unsigned* stack;
     LogEnt* log;
     Inst s;
+#if PB_PDES
+    HeapEnt* s_heap;  // per-instance shared-memory heap slots (hs each, 1-based)
+    int hs;
+    long long hcap;   // per-instance HBM heap capacity (n + 2)
+    PeakRec* prec;    // this warp's peak records
+#endif
 };
 
 struct Scal {
@@ -213,6 +253,14 @@ struct Scal {
     int status;
     long long gpu_total, peak, nlog;
     long long events, plans, visits, req_iters, ans_tokens, health, adm_rounds, adm_slow;
+#if PB_PDES
+    long long prec_base;  // gpu_total at this warp's last peak record
+    int prec_n;           // peak records this round
+    int cur_inst;         // instance of the event being processed
+    bool phase_b;         // processing a serialised (cross-instance) event
+    int reason;           // why this warp declined the replica (engine_pdes.cuh kPdes*)
+    long long nb;         // serialised (phase-B) events processed by this warp
+#endif
 };
 
 DEVI uint2* queue_ptr(const Rep& R, int i, int low) {
@@ -264,7 +312,8 @@ __device__ __noinline__ void heap_sift_up(HeapEnt* h, int pos, double t, unsigne
     h[pos].t = t;
     h[pos].key = key;
 }
-DEVI void heap_push(const Rep& R, Scal& S, double t, unsigned kind, unsigned id) {
+#if !PB_PDES
+DEVI void heap_push(const Rep& R, Scal& S, double t, unsigned kind, unsigned id, int /*inst*/) {
     // engine.cpp:85-89
     if (t < S.now - 1e-12) {
         if (S.status == 0) S.status = kErrPast;
@@ -282,11 +331,10 @@ DEVI void heap_push(const Rep& R, Scal& S, double t, unsigned kind, unsigned id)
     if (lane_id() == 0) heap_sift_up(S.heap, pos, t, key);
     __syncwarp();
 }
-DEVI HeapEnt heap_pop(const Rep& R, Scal& S) {
+#endif
+DEVI HeapEnt heap_pop_at(HeapEnt* h, int n) {
     HeapEnt top;
-    int n = S.hn;
     if (lane_id() == 0) {
-        HeapEnt* h = S.heap;
         top = h[1];
         HeapEnt last = h[n];
         int m = n - 1;
@@ -310,10 +358,60 @@ DEVI HeapEnt heap_pop(const Rep& R, Scal& S) {
     }
     top.t = __shfl_sync(FULL, top.t, 0);
     top.key = __shfl_sync(FULL, top.key, 0);
-    S.hn = n - 1;
+    return top;
+}
+#if !PB_PDES
+DEVI HeapEnt heap_pop(const Rep& R, Scal& S) {
+    HeapEnt top = heap_pop_at(S.heap, S.hn);
+    S.hn = S.hn - 1;
     __syncwarp();
     return top;
 }
+#else
+// Per-instance heaps: instance i's heap lives in its shared-memory slots
+// (1-based, hs - 1 usable) until it outgrows them, then in its HBM region of
+// hcap = n + 2 entries. Keys carry the instance's own event counter: within
+// one instance, pushes happen in the same relative order as in the serial
+// engine, so (time, key) orders an instance's events exactly as the global
+// (time, seq) does.
+DEVI HeapEnt* inst_heap(const Rep& R, int i) {
+    return R.s.hspill[i] ? R.heap + (long long)i * R.hcap : R.s_heap + (long long)i * R.hs;
+}
+DEVI void heap_push(const Rep& R, Scal& S, double t, unsigned kind, unsigned id, int inst) {
+    if (t < S.now - 1e-12) {  // engine.cpp:85-89
+        if (S.status == 0) S.status = kErrPast;
+        return;
+    }
+    const int hn = R.s.hn[inst];
+    const bool spilled = R.s.hspill[inst] != 0;
+    const unsigned long long sq = R.s.evseq[inst] + 1;
+    if (hn + 1 >= R.hcap) {
+        if (S.status == 0) S.status = kErrHeap;
+        return;
+    }
+    HeapEnt* h = spilled ? R.heap + (long long)inst * R.hcap : R.s_heap + (long long)inst * R.hs;
+    if (!spilled && hn + 1 >= R.hs) {
+        h = R.heap + (long long)inst * R.hcap;
+        heap_spill(h, R.s_heap + (long long)inst * R.hs, hn);
+    }
+    __syncwarp();
+    if (lane_id() == 0) {
+        heap_sift_up(h, hn + 1, t, (sq << 29) | ((unsigned long long)kind << 26) | id);
+        R.s.hn[inst] = hn + 1;
+        R.s.evseq[inst] = sq;
+        if (!spilled && hn + 1 >= R.hs) R.s.hspill[inst] = 1;
+    }
+    __syncwarp();
+}
+DEVI HeapEnt heap_pop_inst(const Rep& R, int i) {
+    const int n = R.s.hn[i];
+    HeapEnt top = heap_pop_at(inst_heap(R, i), n);
+    __syncwarp();
+    if (lane_id() == 0) R.s.hn[i] = n - 1;
+    __syncwarp();
+    return top;
+}
+#endif
 
 // ------------------------------------------------------------ queues
 // Queue (instance i, class low) is an append-only array of {idx, seq}; an
@@ -351,6 +449,34 @@ DEVI void queue_compact(const Rep& R, int i, int low) {
     __syncwarp();
 }
 
+// Enqueue sequence numbers (engine.cpp:114, instance.cpp:49). The queues rely
+// on two properties only: seqs are unique (an entry is live iff it carries
+// its request's current seq) and ascending in each queue (queue order ==
+// priority order). Serial: one counter per replica. PDES: per-instance
+// counters k, seq = k * ni + i, unique across instances and ascending within
+// each instance's queues. seq_reserve hands out `cnt` seqs on instance i and
+// returns a base for seq_of(R, i, base, r), r in [0, cnt).
+DEVI unsigned seq_reserve(const Rep& R, Scal& S, int i, int cnt) {
+#if PB_PDES
+    const unsigned base = R.s.enq[i];
+    __syncwarp();
+    if (lane_id() == 0) R.s.enq[i] = base + (unsigned)cnt;
+    __syncwarp();
+    return base;
+#else
+    const unsigned base = S.enq;
+    S.enq += (unsigned)cnt;
+    return base;
+#endif
+}
+DEVI unsigned seq_of(const Rep& R, int i, unsigned base, int r) {
+#if PB_PDES
+    return (base + 1u + (unsigned)r) * (unsigned)R.ni + (unsigned)i;
+#else
+    return base + 1u + (unsigned)r;
+#endif
+}
+
 // engine.cpp:111-116 (+ monitor counters r_i / a_i kept incrementally)
 DEVI void enqueue(const Rep& R, Scal& S, int i, int idx, bool high) {
     int len = high ? R.s.hi_len[i] : R.s.lo_len[i];
@@ -358,7 +484,8 @@ DEVI void enqueue(const Rep& R, Scal& S, int i, int idx, bool high) {
         queue_compact(R, i, high ? 0 : 1);
         len = high ? R.s.hi_len[i] : R.s.lo_len[i];
     }
-    unsigned seq = ++S.enq;
+    const unsigned seq = seq_of(R, i, seq_reserve(R, S, i, 1), 0);
+    __syncwarp();  // every lane has read the queue length before lane 0 bumps it
     if (lane_id() == 0) {
         int4 h = R.rs[idx].h;
         h.z = (int)seq;
@@ -366,6 +493,10 @@ DEVI void enqueue(const Rep& R, Scal& S, int i, int idx, bool high) {
         unsigned m = R.rs[idx].meta;
         m = m_set_owner(m_set_qlow(m, !high), i);
         R.rs[idx].meta = m;
+#if PB_PDES
+        if (m_phase(m) == PH_WAIT || m_phase(m) == PH_REASON)
+            R.s.dmin[i] = min(R.s.dmin[i], (int)m_rem(m));
+#endif
         queue_ptr(R, i, high ? 0 : 1)[len] = make_uint2((unsigned)idx, seq);
         if (high) {
             R.s.hi_len[i] = len + 1;
@@ -568,16 +699,52 @@ DEVI void add_gpu(const Rep& R, Scal& S, int i, long long d) {
 DEVI void add_cpu(const Rep& R, int i, long long d) {
     if (lane_id() == 0) R.s.cpu[i] += d;
 }
-DEVI void note_peak(Scal& S) {  // engine.cpp:75-79
+#if PB_PDES
+// The oracle pre-run's peak of sum_i gpu_used (engine.cpp:75-79) is sampled at
+// event ends in global (time, seq) order. Instances advance concurrently, so
+// each warp records {time, change of the total since its last record,
+// sampled?, instance} and the CTA merges a round's records in time order
+// (pdes_merge_peak). Only the oracle run's peak is ever consumed.
+DEVI void peak_record(const Rep& R, Scal& S, bool sampled) {
+    if (R.policy != kOracle) return;
+    const long long d = S.gpu_total - S.prec_base;
+    if (!sampled && d == 0) return;
+    if (S.prec_n >= kPdesPeakRecs) {
+        if (S.status == 0) S.status = kErrPdes, S.reason = 3;  // kPdesRecs
+        return;
+    }
+    if (lane_id() == 0) {
+        PeakRec pr;
+        pr.t = S.now;
+        pr.d = d;
+        pr.sampled = sampled ? 1 : 0;
+        pr.inst = S.cur_inst;
+        R.prec[S.prec_n] = pr;
+    }
+    S.prec_n++;
+    S.prec_base = S.gpu_total;
+}
+#endif
+DEVI void note_peak(const Rep& R, Scal& S) {  // engine.cpp:75-79
+#if PB_PDES
+    peak_record(R, S, true);
+#else
+    (void)R;
     if (S.gpu_total > S.peak) S.peak = S.gpu_total;
+#endif
 }
 
 // engine.cpp:159-190 (Pascal branch; the caller has already set phase,
 // reasoning_end and logged "transition").
 DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
+#if PB_PDES
+    // reads every instance: only legal while the other instances are paused
+    if (!S.phase_b && S.status == 0) S.status = kErrPdes, S.reason = 5;  // kPdesOrder
+#endif
     unsigned m = R.rs[idx].meta;
     int4 h = R.rs[idx].h;
     int cur = m_owner(m);
+    __syncwarp();  // every lane has read the request before lane 0 dequeues it
     if (lane_id() == 0) dequeue_lane(R, idx, cur, m, h.w);
     __syncwarp();
     int target = select_instance(R, S, SEL_ANSWER);
@@ -592,6 +759,9 @@ DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
         long long tgt_free = R.cap - R.s.gpu[target];
         migrate = !(cur_free >= kv && tgt_free < kv);
     }
+    // every lane has read gpu_used / link before lane 0 updates them
+    const double busy = R.s.link[target];
+    __syncwarp();
     if (!migrate) {
         if (lane_id() == 0) {
             R.rs[idx].qused = 0;
@@ -608,7 +778,6 @@ DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
     if (loc == LOC_GPU || m_swin(m)) add_gpu(R, S, cur, -kv);
     else if (loc == LOC_CPU) add_cpu(R, cur, -kv);
     double dur = transfer_latency(R.prof, kv);
-    double busy = R.s.link[target];
     double start = dmax(S.now, busy);  // cluster.cpp:64-68
     double fin = __dadd_rn(start, dur);
     if (lane_id() == 0) {
@@ -620,7 +789,7 @@ DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
         rc->nmig = 1;
     }
     __syncwarp();
-    heap_push(R, S, fin, EV_TRANSFER, (unsigned)idx);
+    heap_push(R, S, fin, EV_TRANSFER, (unsigned)idx, target);
     emit(R, S, kLMigrate, cur, idx, target);
 }
 
@@ -649,7 +818,7 @@ DEVI void deliver_lane(const Rep& R, double now, int idx, double iter_start) {
         pp->nbp = j + 1;
     }
     pp->dlast = v;
-    if (PB_LOG && (R.flags & kRecordDeliv)) {
+    if ((PB_LOG || PB_PDES) && (R.flags & kRecordDeliv)) {  // records mode (parity dumps)
         R.dig[off + nd] = v;
         R.del[off + nd] = now;
     }
@@ -720,8 +889,10 @@ DEVI void pop_stack(const Rep& R, Adm& A, int s, long long need) {
 // highest position holding a resident KV footprint (-1 if none) and, when
 // `count_q`, the quanta histogram for the partition (lane b: quanta == b).
 DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned& qmin,
-                       unsigned& qmax, int& zero_q, int& rbpos, bool count_q, int& qcnt) {
+                       unsigned& qmax, int& zero_q, int& rbpos, bool count_q, int& qcnt,
+                       unsigned& rem_min) {
     unsigned lmin = 0xffffffffu, lmax = 0;
+    unsigned lrem = 255u;  // PDES: min tokens to a phase boundary over the live entries
     int lzero = 0;
     int lrb = -1;
     uint2* q = queue_ptr(R, i, low);
@@ -778,8 +949,9 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
                 lo_len = R.s.lo_len[i];
             }
             int rank = __popc(dm & lanemask_lt());
+            const unsigned sbase = seq_reserve(R, S, i, nd);
             if (dem) {
-                unsigned seq = S.enq + 1 + rank;
+                unsigned seq = seq_of(R, i, sbase, rank);
                 h.z = (int)seq;
                 h.w = 0;
                 R.rs[e.x].h = h;
@@ -796,12 +968,13 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
                 R.s.lcount[i] += nd;
                 R.s.afresh[i] += nd;
             }
-            S.enq += nd;
             S.nlog += nd;
             __syncwarp();
         }
         bool keep = live && !dem;
         cnd = keep && m_candidate(m);
+        if (PB_PDES && live && (m_phase(m) == PH_WAIT || m_phase(m) == PH_REASON))
+            lrem = min(lrem, m_rem(m));
         // compact the queue in place (tombstones and demoted entries leave)
         unsigned km = __ballot_sync(FULL, keep);
         __syncwarp();
@@ -827,6 +1000,7 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
                 need = h.x + 1;
             }
             if (h.w > 0) flags |= CF_QPOS;
+            if (PB_PDES && m_tnext(m)) flags |= CF_TNEXT;
             int pos = nt + __popc(cm & lanemask_lt());
             R.cand[pos] = make_int4((int)e.x, need, h.x, flags);
             R.tmpq[pos] = (unsigned)h.w;
@@ -848,6 +1022,7 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
     }
     qmin = warp_min_u(lmin);
     qmax = warp_max_u(lmax);
+    if (PB_PDES) rem_min = min(rem_min, warp_min_u(lrem));
     zero_q = warp_sum(lzero);
     rbpos = (int)warp_max_u((unsigned)(lrb + 1)) - 1;
     __syncwarp();
@@ -871,6 +1046,7 @@ DEVI int order_segment(const Rep& R, const int4* src, int4* dst, int s, int e, u
     if (!part) {
         if (src != dst)
             for (int k = s + ln; k < e; k += 32) dst[k] = src[k];
+        __syncwarp();  // the admission pass reads these slots from other lanes
         return rb_in;
     }
     const unsigned lt = lanemask_lt();
@@ -971,6 +1147,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     // segment 0 = high queue, segment 1 = low queue (Pascal class 1); one
     // code copy for both (instruction-cache footprint)
     int nt = 0, z0 = 0, rb0 = -1, rb1 = -1, qc0 = 0, qc1 = 0, c1 = 0;
+    unsigned rem_min = 255u;
     unsigned qmin0 = 0xffffffffu, qmax0 = 0, qmin1 = 0xffffffffu, qmax1 = 0;
     const int segs = pascal ? 2 : 1;
 #pragma unroll 1
@@ -978,7 +1155,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         unsigned qmn, qmx;
         int zq, rbs, qc = 0;
         c1 = nt;
-        gather_queue(R, S, i, sg, nt, qmn, qmx, zq, rbs, by_quanta, qc);
+        gather_queue(R, S, i, sg, nt, qmn, qmx, zq, rbs, by_quanta, qc, rem_min);
         if (sg == 0) {
             qmin0 = qmn, qmax0 = qmx, z0 = zq, rb0 = rbs, qc0 = qc;
         } else {
@@ -986,6 +1163,10 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         }
     }
     if (!pascal) c1 = nt;
+#if PB_PDES
+    __syncwarp();
+    if (lane_id() == 0) R.s.dmin[i] = (int)rem_min;
+#endif
     const int n = nt;
     S.visits += n;
     // priority order: the queue-ordered segments are partitioned into the
@@ -1039,6 +1220,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     int pf = INT_MAX;
     long long bcount = 0, bkv = 0;
     int nsw = 0, nimm = 0, nden = 0;
+    bool tn_batch = false;  // PDES: a batch member's next token ends its reasoning
     const int ln = lane_id();
     for (int base = 0; base < n; base += 32) {
         const int ci_l = base + ln;
@@ -1140,6 +1322,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         const unsigned wm = __ballot_sync(FULL, wt);
         if (wm && pf == INT_MAX) pf = base + __ffs(wm) - 1;
         bcount += __popc(__ballot_sync(FULL, inb));
+        if (PB_PDES && __ballot_sync(FULL, inb && (my_w & CF_TNEXT))) tn_batch = true;
         bkv += inb ? (long long)my.z : 0;  // lane-local; reduced after the loop
         nsw += __popc(__ballot_sync(FULL, sw));
         nimm += __popc(__ballot_sync(FULL, imm));
@@ -1191,7 +1374,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             pm &= pm - 1;
             double t = __shfl_sync(FULL, sd, j);
             int v = __shfl_sync(FULL, vi, j);
-            heap_push(R, S, __dadd_rn(S.now, t), EV_SWAP, (unsigned)v);
+            heap_push(R, S, __dadd_rn(S.now, t), EV_SWAP, (unsigned)v, i);
         }
     }
     __syncwarp();
@@ -1274,7 +1457,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             swm &= swm - 1;
             double t = __shfl_sync(FULL, sd, j);
             int v = __shfl_sync(FULL, c.x, j);
-            heap_push(R, S, __dadd_rn(S.now, t), EV_SWAP, (unsigned)v);
+            heap_push(R, S, __dadd_rn(S.now, t), EV_SWAP, (unsigned)v, i);
         }
     }
     S.nlog = log0 + A.ne + nsw + nimm + nden;
@@ -1292,7 +1475,14 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             R.s.blen[i] = 0;
         }
         __syncwarp();
-        heap_push(R, S, __dadd_rn(S.now, dur), EV_PREFILL, (unsigned)pf_idx);
+#if PB_PDES
+        // a prefill of an R = 0 request with more than one answer token ends
+        // in a Pascal phase boundary (engine.cpp:295-305)
+        if (lane_id() == 0)
+            R.s.gtime[i] = (R.policy == kPascal && sp.y == 0 && sp.z > 1) ? __dadd_rn(S.now, dur)
+                                                                           : CUDART_INF;
+#endif
+        heap_push(R, S, __dadd_rn(S.now, dur), EV_PREFILL, (unsigned)pf_idx, i);
         emit(R, S, kLPrefillStart, i, pf_idx);
     } else if (kind == 2) {
         add_gpu(R, S, i, bcount);  // growth reserved up front (engine.cpp:245)
@@ -1302,12 +1492,16 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             R.s.blen[i] = (int)bcount;
         }
         __syncwarp();
-        heap_push(R, S, __dadd_rn(S.now, dur), EV_ITER, (unsigned)i);
+#if PB_PDES
+        if (lane_id() == 0)
+            R.s.gtime[i] = (R.policy == kPascal && tn_batch) ? __dadd_rn(S.now, dur) : CUDART_INF;
+#endif
+        heap_push(R, S, __dadd_rn(S.now, dur), EV_ITER, (unsigned)i, i);
         emit(R, S, kLDecodeStart, i, -1, (int)bcount);
     }
     __syncwarp();
     if (R.s.gpu[i] > R.cap && S.status == 0) S.status = kErrCapacity;
-    note_peak(S);
+    note_peak(R, S);
 }
 
 // --------------------------------------------------------------- events
@@ -1323,6 +1517,7 @@ DEVI int on_arrival(Rep& R, Scal& S, int idx) {
         unsigned m = 0;
         m = m_set_loc(m, LOC_CPU);
         m = m_set_phase(m, sp.y > 0 ? PH_REASON : PH_ANSWER);
+        if (PB_PDES) m = m_set_rem(m, sp.y);
         if (lane_id() == 0) {
             int4 h = R.rs[idx].h;
             h.x = sp.x;
@@ -1334,7 +1529,10 @@ DEVI int on_arrival(Rep& R, Scal& S, int idx) {
         add_cpu(R, dst, sp.x);
         high = sp.y > 0 ? true : !pascal;
     } else {
-        if (lane_id() == 0) R.rs[idx].meta = m_set_phase(0u, PH_WAIT);
+        // waiting prefill; PDES: the phase boundary is >= max(1, R) iterations away
+        if (lane_id() == 0)
+            R.rs[idx].meta = PB_PDES ? m_set_rem(m_set_phase(0u, PH_WAIT), sp.y > 0 ? sp.y : 1)
+                                     : m_set_phase(0u, PH_WAIT);
         high = true;
     }
     __syncwarp();
@@ -1388,7 +1586,11 @@ DEVI int on_prefill_complete(Rep& R, Scal& S, int idx) {
             if (R.policy == kPascal) pascal_transition(R, S, idx);
         }
     } else {
-        if (lane_id() == 0) R.rs[idx].meta = m_set_phase(m, PH_REASON);
+        if (lane_id() == 0) {
+            unsigned mm = m_set_phase(m, PH_REASON);
+            if (PB_PDES) mm = m_set_rem(mm, sp.y);
+            R.rs[idx].meta = mm;
+        }
         __syncwarp();
     }
     return i;  // every handler ends with maybe_start on this instance
@@ -1497,6 +1699,7 @@ DEVI int on_iteration_complete(Rep& R, Scal& S, int i) {
                     log_put(R, S.nlog + lpos + 1, S.now, kLFinish, i, idx, 0);
                 }
                 if (fresh_lost) atomicSub(&R.s.afresh[i], 1);
+                if (PB_PDES && m_phase(mm) == PH_REASON) mm = m_set_rem(mm, (long long)sp.y - h.y);
                 R.rs[idx].h = hw;
                 if (use_quanta) R.rs[idx].qused = qu;
                 if (mm != m) R.rs[idx].meta = mm;
@@ -1534,6 +1737,7 @@ DEVI int on_iteration_complete(Rep& R, Scal& S, int i) {
 DEVI int on_swap_complete(Rep& R, Scal& S, int idx) {
     unsigned m = R.rs[idx].meta;
     int i = m_owner(m);
+    __syncwarp();  // every lane has read meta before lane 0 rewrites it
     if (lane_id() == 0) {
         unsigned mm = m;
         if (m_swout(m)) mm = m_set_swout(mm, false);
@@ -1551,6 +1755,7 @@ DEVI int on_transfer_complete(Rep& R, Scal& S, int idx) {
     int dst = m_owner(m);
     long long kv = R.rs[idx].h.x;
     bool fits = R.cap - R.s.gpu[dst] >= kv;
+    __syncwarp();  // every lane has read gpu_used / meta before lane 0 updates them
     if (fits) add_gpu(R, S, dst, kv);
     else add_cpu(R, dst, kv);
     if (lane_id() == 0) {
@@ -1563,10 +1768,11 @@ DEVI int on_transfer_complete(Rep& R, Scal& S, int idx) {
     __syncwarp();
     enqueue(R, S, dst, idx, false);
     emit(R, S, kLTransferComplete, dst, idx);
-    note_peak(S);
+    note_peak(R, S);
     return dst;  // every handler ends with maybe_start on this instance
 }
 
+#if !PB_PDES
 // ------------------------------------------------------------ the replica
 template <bool TAIL_FAST>
 DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem, int c_smem,
@@ -1819,6 +2025,12 @@ int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slot
                                                                        h_slots, b_smem);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
+
+#endif  // !PB_PDES
+
+#if PB_PDES
+#include "engine_pdes.cuh"
+#endif
 
 }  // namespace PB_VARIANT
 }  // namespace pb

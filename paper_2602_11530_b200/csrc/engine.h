@@ -52,6 +52,10 @@ struct ReplicaDesc {
     long long batch_base;  // into batch: ni * n entries
     long long heap_base;   // into heap: n + ni + 2 entries
     long long log_base, log_cap;
+    // instance-parallel (PDES) engine only
+    long long pheap_base;  // into heap: ni * (n + 2) entries (per-instance heaps)
+    double lookahead;      // lower bound on the duration of an event that can create a
+                           // cross-instance interaction (Pascal phase boundary)
 };
 
 // Counters the device reports per replica (roofline accounting).
@@ -72,6 +76,8 @@ enum : int {
     kErrCapacity = 3,  // "instance over GPU capacity"       engine.cpp:255-256
     kErrStall = 4,     // "simulation stalled with unfinished requests"  :424
     kErrHeap = 5,      // device heap overflow (internal)
+    kErrPdes = 6,      // instance-parallel engine declined (cross-instance time tie or a
+                       // bounded buffer overflow): the host re-runs the replica serially
 };
 
 // Per-request record, proj/include/pascalsim/metrics.hpp:15-28 (vectors live
@@ -160,6 +166,8 @@ struct Arena {
     unsigned* elist;
     unsigned* stack;
     LogEnt* log;
+    long long wstride;  // PDES: per-warp scratch copies (cand / tmp / tmpq / cstat / elist /
+                        // stack) are wstride entries apart
 };
 
 // Per-replica metric parameters (RunConfig fields used by build_report).
@@ -223,6 +231,29 @@ PB_HD inline int smem_per_warp(int ni, int n_smem, int c_smem, int h_slots = kSm
            smem_cand_bytes(c_smem) + smem_blocked_bytes(b_smem);
 }
 
+// Instance-parallel engine (one CTA per replica, W warps, instance i owned by
+// warp i % W): shared memory = instance state + per-instance scalars
+// (heap size, spill flag, seq counters, pending-global-event time: 32 B) +
+// per-instance heap slots + per warp a candidate scratch and a peak-record
+// buffer + round control.
+constexpr int kPdesMaxWarps = 8;
+constexpr int kPdesPeakRecs = 64;  // peak records per warp per round (oracle runs)
+PB_HD inline int pdes_inst_bytes(int ni, int hs) {
+    return smem_inst_bytes(ni) + ni * 32 + ni * hs * 16;
+}
+struct PeakRec {  // 24 B: {event-end time, change of sum_i gpu_used, sampled, instance}
+    double t;
+    long long d;
+    int sampled, inst;
+};
+PB_HD inline int pdes_warp_bytes(int c_smem) {
+    return smem_cand_bytes(c_smem) + kPdesPeakRecs * (int)sizeof(PeakRec);
+}
+PB_HD inline int pdes_ctl_bytes() { return 512; }
+PB_HD inline int pdes_smem(int ni, int hs, int c_smem, int warps) {
+    return pdes_inst_bytes(ni, hs) + warps * pdes_warp_bytes(c_smem) + pdes_ctl_bytes();
+}
+
 constexpr int kHistBins = 128;  // PASCAL_HIST_BINS
 
 // Host entries (engine.cu / metrics.cu). All enqueue on `stream`.
@@ -236,6 +267,20 @@ int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slot
 namespace nolog {
 int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
                   int warps_per_block, int blocks, void* stream);
+}
+// Instance-parallel engine for few, large replicas (no decision log): one CTA
+// per replica; replicas that return kErrPdes must be re-run serially.
+namespace pdes {
+int launch_engine(const Arena& a, int max_ni, int hs, int c_smem, int warps, int blocks,
+                  void* stream);
+}
+namespace pdes_pascal {
+int launch_engine(const Arena& a, int max_ni, int hs, int c_smem, int warps, int blocks,
+                  void* stream);
+}
+namespace pdes_oracle {
+int launch_engine(const Arena& a, int max_ni, int hs, int c_smem, int warps, int blocks,
+                  void* stream);
 }
 // `nolog` specialised to batches whose replicas all run one policy (Pascal,
 // Oracle — also the capacity pre-run —, FCFS, RR).

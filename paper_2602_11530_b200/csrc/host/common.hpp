@@ -164,6 +164,7 @@ struct Timing {
     double derive_ms = 0, engine_ms = 0, metrics_ms = 0, total_ms = 0, h2d_ms = 0, d2h_ms = 0;
     long long h2d_bytes = 0, d2h_bytes = 0;
     int launches = 0;
+    int instance_parallel = 0;  // policy-run replicas completed by the instance-parallel engine
 };
 Timing& last_timing();
 void release_cached_memory();

@@ -9,6 +9,7 @@
 // with PASCAL_ERR_INTERNAL.
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include <algorithm>
@@ -307,6 +308,9 @@ public:
     int dev_ = -1;  // the device the batch's arenas and stream live on
 
     int n_rep_ = 0, max_ni_ = 1, max_n_ = 0, max_on_ = 0;
+    int pdes_w_ = 0;             // warps per replica of the instance-parallel engine (0: off)
+    long long pheap_total_ = 0;  // per-instance heaps of the instance-parallel engine
+    std::vector<int> declined_;  // replicas the instance-parallel engine handed back
     long long total_req_ = 0, total_ans_ = 0, total_q_ = 0, total_batch_ = 0, total_heap_ = 0,
               total_log_ = 0;
     std::vector<pb::ReplicaDesc> desc_;
@@ -318,7 +322,7 @@ public:
     cudaEvent_t ev_[5] = {};
     DevBuf<pb::ReplicaDesc> d_desc_, d_odesc_, d_desc_init_;
     DevBuf<pb::ReplicaOut> d_out_, d_oout_;
-    DevBuf<int> d_work_, d_omap_, d_oref_, d_rid_, d_order_, d_oorder_;
+    DevBuf<int> d_work_, d_omap_, d_oref_, d_rid_, d_order_, d_oorder_, d_sub_;
     DevBuf<double> d_arrival_, d_frac_;
     DevBuf<int4> d_spec_, d_cand_, d_tmp_;
     DevBuf<pb::ReqState> d_rs_;
@@ -406,7 +410,23 @@ void Batch::build() {
         d.queue_base = q;
         d.batch_base = bt;
         d.heap_base = hp;
+        d.pheap_base = 0;  // set below when the instance-parallel engine is used
         d.log_base = lg;
+        {
+            // lookahead of the instance-parallel engine (engine_pdes.cuh): a
+            // lower bound on the duration of any decode iteration
+            // ((base + per_request * B) + per_kv * K >= base + per_request for
+            // B >= 1, K >= 0; rounding is monotone) and of any prefill that
+            // ends in a phase boundary (R = 0, not preloaded, A > 1).
+            double la = j.prof.decode_base + j.prof.decode_per_request * 1.0;
+            long long pmin = -1;
+            for (const Spec& s : *j.trace)
+                if (s.reasoning == 0 && !s.preloaded && s.answering > 1)
+                    pmin = pmin < 0 ? s.prompt : std::min<long long>(pmin, s.prompt);
+            if (pmin >= 0)
+                la = std::min(la, j.prof.prefill_base + j.prof.prefill_per_token * (double)pmin);
+            d.lookahead = la;
+        }
         d.log_cap = log_cap_;
         long long big = 0;
         for (const Spec& s : *j.trace) big = std::max(big, (long long)s.max_kv());
@@ -464,7 +484,41 @@ void Batch::build() {
         hp += n + ni + 2;
         lg += log_cap_;
     }
+    // Instance-parallel engine: few replicas (latency shapes: each gets a
+    // whole SM), more than one instance, no decision log (record arrays are
+    // kept: records-only parity dumps run on it),
+    // enqueue seqs (k * ni + i) within 32 bits, a positive lookahead for
+    // Pascal. PB_PDES=0 disables it (experiment hook / A-B).
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const char* pe = std::getenv("PB_PDES");
+        bool ok = !(pe && std::atoi(pe) == 0) && log_cap_ == 0 && n_rep_ >= 1 &&
+                  n_rep_ <= sms && max_ni_ >= 2;
+        long long ph = 0;
+        for (int r = 0; ok && r < n_rep_; ++r) {
+            const pb::ReplicaDesc& d = desc_[r];
+            // enqueues per request <= 4 (arrival, demotion, phase boundary, transfer)
+            if ((4.0 * d.n + 8.0) * (double)d.ni >= 4294967295.0) ok = false;
+            if (d.policy == pb::kPascal && !(d.lookahead > 0.0)) ok = false;
+        }
+        if (ok) {
+            pdes_w_ = std::min(pb::kPdesMaxWarps, max_ni_);
+            for (int r = 0; r < n_rep_; ++r) {
+                desc_[r].pheap_base = ph;
+                ph += (long long)desc_[r].ni * (desc_[r].n + 2);
+            }
+            for (pb::ReplicaDesc& od : odesc_) {  // pre-runs share their replica's layout
+                for (int r = 0; r < n_rep_; ++r)
+                    if (desc_[r].req_base == od.req_base) od.pheap_base = desc_[r].pheap_base;
+            }
+            pheap_total_ = ph;
+        }
+    }
     seg[n_rep_] = rq;
+    if (rq > (long long)INT_MAX)  // the per-replica TTFT sort (CUB) counts items in int
+        throw std::invalid_argument("batch exceeds 2^31 - 1 requests in total; split it");
     total_req_ = rq;
     total_ans_ = ans;
     total_q_ = q;
@@ -510,12 +564,15 @@ void Batch::build() {
     d_aoff32_.ensure(rq);
     d_blocked_.ensure(rq);
     d_rec_.ensure(rq);
-    d_cand_.ensure(rq);
-    d_tmp_.ensure(rq);
-    d_tmpq_.ensure(rq);
-    d_cstat_.ensure(rq);
-    d_elist_.ensure(rq);
-    d_stack_.ensure(rq);
+    // per-warp planner scratch: one copy per warp of a replica under the
+    // instance-parallel engine
+    const long long scr = rq * std::max(1, pdes_w_);
+    d_cand_.ensure(scr);
+    d_tmp_.ensure(scr);
+    d_tmpq_.ensure(scr);
+    d_cstat_.ensure(scr);
+    d_elist_.ensure(scr);
+    d_stack_.ensure(scr);
     d_ph_.ensure(rq);
     d_bpv_.ensure(ans);
     d_bpk_.ensure(ans);
@@ -523,7 +580,7 @@ void Batch::build() {
     d_del_.ensure(records_ ? ans : 1);
     d_qent_.ensure(q);
     d_batch_.ensure(bt);
-    d_heap_.ensure(hp);
+    d_heap_.ensure(std::max(hp, pheap_total_));
     d_log_.ensure(std::max<long long>(lg, 1));
     d_params_.ensure(n_rep_);
     d_frac_.ensure(n_rep_);
@@ -628,6 +685,7 @@ pb::Arena Batch::arena(bool oracle) const {
     a.elist = d_elist_.p;
     a.stack = d_stack_.p;
     a.log = d_log_.p;
+    a.wstride = total_req_;
     return a;
 }
 
@@ -663,25 +721,88 @@ void Batch::execute() {
                    st_);
     };
     int launches = 0;
+    // Instance-parallel engine (engine_pdes.cuh) for few, large replicas; the
+    // replicas it declines (kErrPdes) are re-run by the serial engine on the
+    // same stream before anything reads their results.
+    using PLauncher = int (*)(const pb::Arena&, int, int, int, int, int, void*);
+    auto run = [&](bool pre_run) {
+        pb::Arena ar = arena(pre_run);
+        const int reps = ar.n_rep;
+        const int max_n = pre_run ? max_on_ : max_n_;
+        if (pdes_w_ == 0) {
+            if (!pre_run) tm.instance_parallel = 0;
+            if (launch(ar, reps, max_n, pre_run))
+                throw std::logic_error(pre_run ? "engine launch failed (oracle pre-run)"
+                                               : "engine launch failed");
+            launches += 1;
+            return;
+        }
+        int dev = 0, sms = 148, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        const int budget = std::max(48 * 1024, optin) - 1024;
+        int c = std::max(32, std::min(max_n, 512)), hs = 32;
+        while (pb::pdes_smem(max_ni_, hs, c, pdes_w_) > budget && c > 32) c /= 2;
+        while (pb::pdes_smem(max_ni_, hs, c, pdes_w_) > budget && hs > 4) hs /= 2;
+        PLauncher eng = pre_run ? (spec ? pb::pdes_oracle::launch_engine : pb::pdes::launch_engine)
+                                : (spec && common == pb::kPascal ? pb::pdes_pascal::launch_engine
+                                                                 : pb::pdes::launch_engine);
+        if (eng(ar, max_ni_, hs, c, pdes_w_, std::min(reps, sms), st_))
+            throw std::logic_error("instance-parallel engine launch failed");
+        launches += 1;
+        std::vector<pb::ReplicaOut> outs(reps);
+        ck(cudaMemcpyAsync(outs.data(), ar.out, reps * sizeof(pb::ReplicaOut),
+                           cudaMemcpyDeviceToHost, st_),
+           "d2h");
+        ck(cudaStreamSynchronize(st_), "instance-parallel engine");
+        std::vector<int> sub;
+        static const bool dbg = std::getenv("PB_PDES_DEBUG") != nullptr;
+        if (dbg)
+            for (int r = 0; r < std::min(reps, 4); ++r)
+                std::fprintf(stderr, "[pdes] %s replica %d: events %lld rounds %.0f serialised %lld\n",
+                             pre_run ? "oracle" : "policy", r, outs[r].events, outs[r].now,
+                             outs[r].nlog);
+        for (int r = 0; r < reps; ++r)
+            if (outs[r].status == pb::kErrPdes) {
+                sub.push_back(r);
+                if (dbg)  // ReplicaOut::pad carries the decline reason (engine_pdes.cuh)
+                    std::fprintf(stderr, "[pdes] %s replica %d declined, reason %d\n",
+                                 pre_run ? "oracle" : "policy", r, outs[r].pad);
+            }
+        if (!pre_run) {
+            declined_ = sub;
+            tm.instance_parallel = reps - (int)sub.size();
+        }
+        if (sub.empty()) return;
+        d_sub_.ensure(sub.size());
+        ck(cudaMemcpyAsync(d_sub_.p, sub.data(), sub.size() * sizeof(int), cudaMemcpyHostToDevice,
+                           st_),
+           "h2d");
+        ck(cudaMemsetAsync(const_cast<int*>(ar.work), 0, sizeof(int), st_), "memset");
+        pb::Arena sa = ar;
+        sa.order = d_sub_.p;
+        sa.n_rep = (int)sub.size();
+        if (launch(sa, sa.n_rep, max_n, pre_run))
+            throw std::logic_error("engine launch failed (serial re-run)");
+        launches += 1;
+        ck(cudaStreamSynchronize(st_), "serial re-run");  // d_sub_ is reused by the next run
+    };
     ck(cudaEventRecord(ev_[0], st_), "event");
     ck(cudaMemcpyAsync(d_desc_.p, d_desc_init_.p, n_rep_ * sizeof(pb::ReplicaDesc),
                        cudaMemcpyDeviceToDevice, st_),
        "desc reset");
     ck(cudaMemsetAsync(d_work_.p, 0, 2 * sizeof(int), st_), "memset");
     if (!odesc_.empty()) {
-        pb::Arena oa = arena(true);
-        if (launch(oa, (int)odesc_.size(), max_on_, true))
-            throw std::logic_error("engine launch failed (oracle pre-run)");
+        run(true);
         if (pb::launch_capacity(d_desc_.p, d_oout_.p, d_omap_.p, d_oref_.p, d_frac_.p,
                                 d_biggest_.p, d_echo_.p, (int)omap_.size(), st_))
             throw std::logic_error("capacity kernel launch failed");
-        launches += 2;
+        launches += 1;
     }
     ck(cudaEventRecord(ev_[1], st_), "event");
     pb::Arena pa = arena(false);
-    if (launch(pa, n_rep_, max_n_, false))
-        throw std::logic_error("engine launch failed");
-    launches += 1;
+    run(false);
     ck(cudaEventRecord(ev_[2], st_), "event");
     pb::RowArrays rows{d_ttft_.p, d_ttfat_.p, d_qoe_.p, d_block_.p, d_slo_.p, d_sorted_.p};
     size_t bytes = sort_bytes_;

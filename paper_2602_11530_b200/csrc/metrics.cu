@@ -13,6 +13,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 
 #include <cub/device/device_segmented_sort.cuh>
@@ -175,6 +176,40 @@ __global__ void summary_kernel(const MetricParams* params, const ReplicaDesc* de
 
 // Per-group TTFT histogram + SLO counters over all requests of the group's
 // replicas (the sweep's device-side reduction; merged across GPUs by NCCL).
+// Counters are privatised per CTA in shared memory (32-bit) and flushed once
+// per CTA with 64-bit global atomics on the non-zero bins only; a batch's
+// requests are grouped by replica, so a CTA's requests fall in few groups and
+// the flush is a few hundred atomics instead of three per request.
+__device__ __forceinline__ int ttft_bin(double t) {
+    if (!(t >= 1e-4)) return 0;
+    if (t >= 1e5) return kHistBins + 1;
+    return 1 + min(kHistBins - 1, (int)((log10(t) + 4.0) * (kHistBins / 9.0)));
+}
+
+__global__ void hist_smem_kernel(const int* rid, const int* group, RowArrays rows,
+                                 const ReplicaOut* out, long long total, int n_groups,
+                                 unsigned long long* hist, unsigned long long* slo) {
+    extern __shared__ unsigned sh[];  // [n_groups][kHistBins + 2] then [n_groups][2]
+    const int nh = n_groups * (kHistBins + 2), ns = 2 * n_groups;
+    for (int k = threadIdx.x; k < nh + ns; k += blockDim.x) sh[k] = 0u;
+    __syncthreads();
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += stride) {
+        const int r = rid[g];
+        if (out[r].status != 0) continue;
+        const int grp = group[r];
+        atomicAdd(&sh[grp * (kHistBins + 2) + ttft_bin(rows.ttft[g])], 1u);
+        if (rows.slo[g]) atomicAdd(&sh[nh + 2 * grp], 1u);
+        atomicAdd(&sh[nh + 2 * grp + 1], 1u);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nh; k += blockDim.x)
+        if (sh[k]) atomicAdd(&hist[k], (unsigned long long)sh[k]);
+    for (int k = threadIdx.x; k < ns; k += blockDim.x)
+        if (sh[nh + k]) atomicAdd(&slo[k], (unsigned long long)sh[nh + k]);
+}
+
+// Fallback for group counts whose counters do not fit in shared memory.
 __global__ void hist_kernel(const int* rid, const int* group, RowArrays rows,
                             const ReplicaOut* out, long long total, unsigned long long* hist,
                             unsigned long long* slo) {
@@ -183,12 +218,7 @@ __global__ void hist_kernel(const int* rid, const int* group, RowArrays rows,
     const int r = rid[g];
     if (out[r].status != 0) return;
     const int grp = group[r];
-    const double t = rows.ttft[g];
-    int bin;
-    if (!(t >= 1e-4)) bin = 0;
-    else if (t >= 1e5) bin = kHistBins + 1;
-    else bin = 1 + min(kHistBins - 1, (int)((log10(t) + 4.0) * (kHistBins / 9.0)));
-    atomicAdd(&hist[(long long)grp * (kHistBins + 2) + bin], 1ull);
+    atomicAdd(&hist[(long long)grp * (kHistBins + 2) + ttft_bin(rows.ttft[g])], 1ull);
     atomicAdd(&slo[2 * grp], (unsigned long long)rows.slo[g]);
     atomicAdd(&slo[2 * grp + 1], 1ull);
 }
@@ -199,9 +229,27 @@ int launch_histograms(const int* rid, const int* group, const RowArrays rows,
     cudaStream_t st = (cudaStream_t)stream;
     cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * n_groups * (kHistBins + 2), st);
     cudaMemsetAsync(slo, 0, sizeof(unsigned long long) * n_groups * 2, st);
-    if (total > 0)
-        hist_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(rid, group, rows, out, total,
-                                                                     hist, slo);
+    if (total > 0) {
+        const size_t smem = sizeof(unsigned) * (size_t)n_groups * (kHistBins + 4);
+        if (smem <= 96 * 1024) {
+            static bool attr = false;  // opt in above 48 KB once per process
+            if (!attr) {
+                cudaFuncSetAttribute(hist_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     96 * 1024);
+                attr = true;
+            }
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const long long want = (total + 1023) / 1024;
+            const int blocks = (int)std::min<long long>(want, 2ll * sms);
+            hist_smem_kernel<<<blocks, 512, smem, st>>>(rid, group, rows, out, total, n_groups,
+                                                       hist, slo);
+        } else {
+            hist_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(rid, group, rows, out,
+                                                                         total, hist, slo);
+        }
+    }
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -219,6 +267,9 @@ int launch_metrics(const Arena& a, const MetricParams* params, const long long* 
                    DevSummary* out, const long long* echo_capacity, void* sort_tmp,
                    size_t* sort_tmp_bytes, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    // CUB's segmented sort counts items in int; Batch::build rejects larger
+    // batches (engine_host.cpp), this is the backstop
+    if (total > (long long)INT_MAX) return 4;
     if (sort_tmp == nullptr) {  // size query
         size_t bytes = 0;
         cudaError_t e = cub::DeviceSegmentedSort::SortKeys(

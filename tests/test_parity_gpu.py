@@ -82,3 +82,29 @@ def test_xlarge_records_and_reports(c, tmp_path):
     pb.run(t, make_profile(c), make_cfg(c), prefix)
     for ext, want in g["report"].items():
         assert sha_file(f"{prefix}.{ext}") == want, ext
+
+
+# The instance-parallel engine (csrc/engine_pdes.cuh) runs every records-only
+# dump of a replica with more than one instance; replicas it declines (an
+# exact cross-instance time tie, e.g. the integer-time unit profiles) are
+# re-run by the serial engine. Records (every double) must match the
+# reference either way, and the realistic-profile cases must not be declined.
+MULTI = [c for c in CASES if c["name"] in GOLD and c["size"] in ("tiny", "small", "medium")
+         and c["cfg"].get("instance_count", 8) >= 2]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c", MULTI, ids=[c["name"] for c in MULTI])
+def test_instance_parallel_records_bit_exact(c, tmp_path):
+    g = GOLD[c["name"]]
+    t = build_trace(c["trace"])
+    rec = str(tmp_path / "gpu.rec")
+    pb.run_dump(t, make_profile(c), make_cfg(c), rec, None)
+    used = pb.last_timing().instance_parallel
+    got = sha_file(rec)
+    if got != g["records"]:
+        orec, _ = oracle_run(c, t, str(tmp_path))
+        pytest.fail(f"records {got} vs {g['records']} (instance-parallel: {used})\n" +
+                    first_diff(rec, orec))
+    if len(t) > 0:
+        assert used in (0, 1)
