@@ -32,7 +32,22 @@ typedef struct {
     long long admission_slow_steps; /* candidates decided by the exact scalar step */
     int status;                    /* pascal_status of this replica */
     int pad;
+    /* time per output token, not a reference output: per request
+     * (completion - first answer delivery) / (A - 1) for A > 1 answer tokens;
+     * the mean over those requests, and how many there are */
+    double tpot_mean;
+    long long tpot_requests;
 } pascal_summary;
+
+/* One request's latency-model outputs (metrics::RequestRow,
+ * proj/include/pascalsim/metrics.hpp:58-67) plus its TPOT. */
+typedef struct {
+    long id;
+    double ttft, ttfat, qoe, blocking_latency;
+    double tpot; /* (completion - first answer delivery) / (A - 1); 0 when A <= 1 */
+    int slo_violated;
+    int pad;
+} pascal_request_row;
 
 /* Device-side timing of the most recent batch execution on this thread. */
 typedef struct {
@@ -61,6 +76,9 @@ pascal_status pascal_batch_execute(pascal_batch* b);
 /* Copies the per-replica summaries to host memory. */
 pascal_status pascal_batch_summaries(pascal_batch* b, pascal_summary* out);
 void pascal_batch_free(pascal_batch* b);
+/* Per-request rows of replica `replica` after an execute, trace order;
+ * `out` holds pascal_trace_size(trace of that replica) entries. */
+pascal_status pascal_batch_rows(pascal_batch* b, size_t replica, pascal_request_row* out);
 
 /* Sweep reduction on the device: per-group TTFT histograms over every request
  * of the group's replicas (PASCAL_HIST_BINS log-spaced bins over
@@ -125,6 +143,78 @@ long long pascal_trace_request_iterations(const pascal_trace* t);
  * (on every device). Blocks in use by live batches are not affected. The
  * idle cache is also bounded by PB_POOL_CACHE_MB (default 16384) per device. */
 pascal_status pascal_release_cached_memory(void);
+
+/* ---- Unit-parity seams ------------------------------------------------
+ * The reference keeps its planner and placement rules as pure C++ functions
+ * that its unit tests drive with hand-built states: instance::apply_demotion
+ * + instance::plan_iteration + the plan application in Simulator::maybe_start
+ * (proj/src/instance.cpp:39-57,103-282, proj/src/engine.cpp:192-258;
+ * fixtures proj/tests/test_instance.cpp:84-306) and
+ * cluster::select_instance_reasoning / _answering / route_arrival
+ * (proj/src/cluster.cpp:27-44,59-62; proj/tests/test_cluster.cpp:67-107,
+ * proj/tests/acceptance.cpp:137-216). The device engine fuses them into its
+ * event loop; these entries run the engine's own code (the same inlined
+ * planner and the same select_instance) for one step on a hand-built state,
+ * on the current device. */
+
+/* RequestState (proj/include/pascalsim/instance.hpp:41-62); request k's id is
+ * k and requests must be in arrival order (as a trace is). */
+typedef struct {
+    double arrival_time;
+    long prompt_tokens, reasoning_tokens, answering_tokens;
+    int phase;        /* 0 WaitingPrefill, 1 Reasoning, 2 Answering, 4 Done (Phase) */
+    int kv_location;  /* 0 Gpu, 1 Cpu, 2 InTransit (KvLocation) */
+    int swapping_in, swapping_out;
+    long tokens_generated, kv_tokens, quantum_used_in_round, quanta_exhausted;
+    unsigned long long enqueue_seq;
+} pascal_probe_request;
+
+/* InstanceState (instance.hpp:74-88) of the instance being planned, plus the
+ * engine inputs maybe_start reads: policy, demotion threshold, the enqueue
+ * counter demotions draw from, and the clock. */
+typedef struct {
+    const pascal_probe_request* requests;
+    long n_requests;
+    const long* high_queue;
+    long n_high;
+    const long* low_queue;
+    long n_low;
+    long gpu_capacity, gpu_used, cpu_used;
+    unsigned long long enqueue_counter;
+    long demotion_threshold;
+    const char* policy; /* "fcfs" | "rr" | "oracle" | "pascal" */
+    double now;
+    int candidate_scratch; /* device shared-memory candidate slots (0: all in HBM) */
+} pascal_probe_state;
+
+/* What maybe_start did, in the reference's order. List arrays are caller
+ * buffers of n_requests entries (NULL to skip); the counts are always set.
+ * Completion / swap event times are the times the step pushed
+ * (now + duration), as the event queue holds them. */
+typedef struct {
+    int kind;           /* 0 Idle, 1 Prefill, 2 Decode (IterationPlan::Kind) */
+    int over_capacity;  /* "instance over GPU capacity" (engine.cpp:255-256) fired */
+    long prefill_request;
+    double completion_time; /* PrefillComplete / IterationComplete time; 0 when idle */
+    long gpu_used, cpu_used;
+    long *demoted, *evictions, *swap_ins, *immediate_swap_ins, *denied, *batch;
+    long n_demoted, n_evictions, n_swap_ins, n_immediate_swap_ins, n_denied, n_batch;
+    long* swap_event_request;  /* SwapComplete pushes, in push order */
+    double* swap_event_time;
+    long n_swap_events;
+    double* blocked;           /* per request: blocked time this step added */
+} pascal_probe_plan;
+
+pascal_status pascal_probe_maybe_start(const pascal_probe_state* st, const pascal_profile* p,
+                                       pascal_probe_plan* out);
+
+/* `count` snapshot vectors of n instances each (n <= 32), instance i of
+ * vector v at v*n+i: on_track = t_i, key1 = m_i (modes 0, 2) or r_i (mode 1),
+ * key2 = a_i (mode 1). mode 0: select_instance_reasoning (Alg. 1), 1:
+ * select_instance_answering (Alg. 2), 2: baseline route_arrival (argmin
+ * m_i). Writes the chosen instance of every vector to out[v]. */
+pascal_status pascal_probe_select(int mode, long count, int n, const unsigned char* on_track,
+                                  const long* key1, const long* key2, int* out);
 
 /* One process per GPU: selects the CUDA device for this thread. */
 pascal_status pascal_set_device(int device);

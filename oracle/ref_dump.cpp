@@ -42,7 +42,9 @@
 #include <string>
 #include <vector>
 
+#include "pascalsim/cluster.hpp"
 #include "pascalsim/engine.hpp"
+#include "pascalsim/instance.hpp"
 #include "pascalsim/metrics.hpp"
 #include "pascalsim/workload.hpp"
 
@@ -155,6 +157,178 @@ struct FileBuf : std::streambuf {
     }
 };
 
+// ---- unit parity: one maybe_start step on a hand-built state -------------
+// STATE lines:  policy P | capacity C | gpu_used G | cpu_used U | counter K |
+//   demotion D | now T(%a) | prof KEY VALUE | req ARRIVAL(%a) PROMPT REASONING
+//   ANSWERING PHASE LOC SWIN SWOUT TOKENS KV QUSED QUANTA SEQ | high IDX... |
+//   low IDX...   (request k has id k)
+int plan_state(const std::string& path) {
+    using namespace instance;
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("cannot open " + path);
+    InstanceState st;
+    std::vector<RequestState> reqs;
+    costmodel::LatencyProfile prof;
+    Policy policy = Policy::Pascal;
+    std::uint64_t counter = 0;
+    double now = 0.0;
+    std::string line;
+    while (std::getline(in, line)) {
+        std::istringstream ls(line);
+        std::string k;
+        ls >> k;
+        if (k == "policy") {
+            std::string v;
+            ls >> v;
+            policy = engine::parse_policy(v);
+        } else if (k == "capacity") ls >> st.gpu_capacity;
+        else if (k == "gpu_used") ls >> st.gpu_used;
+        else if (k == "cpu_used") ls >> st.cpu_used;
+        else if (k == "counter") ls >> counter;
+        else if (k == "demotion") ls >> st.demotion_threshold;
+        else if (k == "now") {
+            std::string v;
+            ls >> v;
+            now = std::strtod(v.c_str(), nullptr);
+        } else if (k == "prof") {
+            std::string f, v;
+            ls >> f >> v;
+            costmodel::profile_set_field(prof, f, std::strtod(v.c_str(), nullptr));
+        } else if (k == "req") {
+            RequestState r;
+            std::string arr;
+            int phase = 0, loc = 0, sin = 0, sout = 0;
+            ls >> arr >> r.spec.prompt_tokens >> r.spec.reasoning_tokens >>
+                r.spec.answering_tokens >> phase >> loc >> sin >> sout >> r.tokens_generated >>
+                r.kv_tokens >> r.quantum_used_in_round >> r.quanta_exhausted >> r.enqueue_seq;
+            r.spec.id = static_cast<long>(reqs.size());
+            r.spec.arrival_time = std::strtod(arr.c_str(), nullptr);
+            r.phase = static_cast<Phase>(phase);
+            r.kv_location = static_cast<KvLocation>(loc);
+            r.swapping_in = sin != 0;
+            r.swapping_out = sout != 0;
+            r.owner = 0;
+            reqs.push_back(r);
+        } else if (k == "high" || k == "low") {
+            long idx;
+            while (ls >> idx) (k == "high" ? st.high_queue : st.low_queue).push_back(idx);
+        }
+    }
+    auto list = [](const char* tag, const std::vector<long>& v) {
+        std::printf("%s", tag);
+        for (long x : v) std::printf(" %ld", x);
+        std::printf("\n");
+    };
+    // Simulator::maybe_start (proj/src/engine.cpp:192-258) minus emit/push:
+    // pushes are printed as (request, time) in push order.
+    std::vector<long> demoted;
+    if (policy == Policy::Pascal) demoted = apply_demotion(st, reqs, counter);
+    IterationPlan plan = plan_iteration(st, reqs, prof, policy, now);
+    std::vector<std::pair<long, double>> swap_events;
+    for (long v : plan.evictions) {
+        RequestState& r = reqs[static_cast<std::size_t>(v)];
+        st.gpu_used -= r.kv_tokens;
+        st.cpu_used += r.kv_tokens;
+        r.kv_location = KvLocation::Cpu;
+        double dur = costmodel::swap_latency(prof, r.kv_tokens);
+        if (dur > 0.0) {
+            r.swapping_out = true;
+            swap_events.emplace_back(v, now + dur);
+        }
+    }
+    for (long s : plan.swap_ins) {
+        RequestState& r = reqs[static_cast<std::size_t>(s)];
+        st.cpu_used -= r.kv_tokens;
+        st.gpu_used += r.kv_tokens;
+        r.swapping_in = true;
+        swap_events.emplace_back(s, now + costmodel::swap_latency(prof, r.kv_tokens));
+    }
+    for (long s : plan.immediate_swap_ins) {
+        RequestState& r = reqs[static_cast<std::size_t>(s)];
+        st.cpu_used -= r.kv_tokens;
+        st.gpu_used += r.kv_tokens;
+        r.kv_location = KvLocation::Gpu;
+    }
+    double completion = 0.0;
+    int kind = 0;
+    if (plan.kind == IterationPlan::Kind::Prefill) {
+        RequestState& r = reqs[static_cast<std::size_t>(plan.prefill_request)];
+        long extra = r.spec.reasoning_tokens == 0 ? 1 : 0;
+        st.gpu_used += r.spec.prompt_tokens + extra;
+        completion = now + plan.duration;
+        kind = 1;
+    } else if (plan.kind == IterationPlan::Kind::Decode) {
+        st.gpu_used += static_cast<long>(plan.batch.size());
+        completion = now + plan.duration;
+        kind = 2;
+    }
+    list("demoted", demoted);
+    list("evict", plan.evictions);
+    list("swapin", plan.swap_ins);
+    list("immediate", plan.immediate_swap_ins);
+    list("denied", plan.denied);
+    std::printf("kind %d prefill %ld\n", kind, kind == 1 ? plan.prefill_request : -1L);
+    list("batch", kind == 2 ? plan.batch : std::vector<long>{});
+    std::printf("used %ld %ld\n", st.gpu_used, st.cpu_used);
+    std::printf("completion %a\n", completion);
+    std::printf("swapev");
+    for (auto& [id, t] : swap_events) std::printf(" %ld %a", id, t);
+    std::printf("\n");
+    // rec(d).blocked_interval_total += plan.duration, from 0
+    std::printf("blocked %a\n", plan.denied.empty() ? 0.0 : 0.0 + plan.duration);
+    std::printf("over %d\n", st.gpu_used > st.gpu_capacity ? 1 : 0);
+    return 0;
+}
+
+// acceptance.cpp criterion 2's vectors (proj/tests/acceptance.cpp:168-216).
+int select_vectors(const std::string& out) {
+    std::vector<unsigned char> bytes;
+    using instance::MonitorSnapshot;
+    for (int pass = 0; pass < 2; ++pass) {  // 0: Alg. 1, 1: baseline argmin m
+        for (int n = 1; n <= 4; ++n) {
+            long combos = 1;
+            for (int i = 0; i < n; ++i) combos *= 8;
+            for (long code = 0; code < combos; ++code) {
+                long c = code;
+                std::vector<MonitorSnapshot> snaps(static_cast<std::size_t>(n));
+                for (int i = 0; i < n; ++i) {
+                    snaps[i].instance_id = i;
+                    snaps[i].all_answering_on_track = (c % 2) != 0;
+                    c /= 2;
+                    snaps[i].total_kv = c % 4;
+                    c /= 4;
+                }
+                int id = pass == 0 ? cluster::select_instance_reasoning(snaps)
+                                   : cluster::route_arrival(snaps, instance::Policy::Fcfs);
+                bytes.push_back(static_cast<unsigned char>(id));
+            }
+        }
+    }
+    for (int n = 1; n <= 4; ++n) {
+        long combos = 1;
+        for (int i = 0; i < n; ++i) combos *= 32;
+        for (long code = 0; code < combos; ++code) {
+            long c = code;
+            std::vector<MonitorSnapshot> snaps(static_cast<std::size_t>(n));
+            for (int i = 0; i < n; ++i) {
+                snaps[i].instance_id = i;
+                snaps[i].all_answering_on_track = (c % 2) != 0;
+                c /= 2;
+                snaps[i].reasoning_count = c % 4;
+                c /= 4;
+                snaps[i].fresh_answering_count = c % 4;
+                c /= 4;
+            }
+            bytes.push_back(static_cast<unsigned char>(cluster::select_instance_answering(snaps)));
+        }
+    }
+    FILE* f = std::fopen(out.c_str(), "wb");
+    if (!f) throw std::runtime_error("cannot write " + out);
+    std::fwrite(bytes.data(), 1, bytes.size(), f);
+    std::fclose(f);
+    return 0;
+}
+
 int usage() {
     std::fprintf(stderr, "usage: see header of oracle/ref_dump.cpp\n");
     return 2;
@@ -260,6 +434,10 @@ int main(int argc, char** argv) {
             std::printf("{\"capacity\": %ld, \"derive_s\": %.3f, \"run_s\": %.3f}\n", cap,
                         std::chrono::duration<double>(t1 - t0).count(),
                         std::chrono::duration<double>(t2 - t1).count());
+        } else if (mode == "plan" && argc == 3) {
+            return plan_state(argv[2]);
+        } else if (mode == "select" && argc == 3) {
+            return select_vectors(argv[2]);
         } else if (mode == "report" && argc == 5) {
             auto t = read_hex_trace(argv[2]);
             Cfg c = read_cfg(argv[3]);

@@ -10,6 +10,8 @@ from .api import (  # noqa: F401
     Trace,
     compare,
     derive_capacity,
+    probe_maybe_start,
+    probe_select,
     device_available,
     last_timing,
     run,

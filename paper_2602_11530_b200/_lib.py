@@ -30,6 +30,7 @@ ABI_SYMBOLS = (
     "pascal_device_available", "pascal_release_cached_memory", "pascal_batch_set_groups",
     "pascal_batch_histograms",
     "pascal_sweep",
+    "pascal_probe_maybe_start", "pascal_probe_select", "pascal_batch_rows",
 )
 HIST_BINS = 128
 
@@ -68,6 +69,17 @@ class Summary(C.Structure):
         ("slo_violations", C.c_longlong),
         ("admission_rounds", C.c_longlong), ("admission_slow_steps", C.c_longlong),
         ("status", C.c_int), ("pad", C.c_int),
+        ("tpot_mean", C.c_double), ("tpot_requests", C.c_longlong),
+    ]
+
+
+class RequestRow(C.Structure):
+    """pascal_request_row (include/pascal_b200.h)."""
+
+    _fields_ = [
+        ("id", C.c_long), ("ttft", C.c_double), ("ttfat", C.c_double), ("qoe", C.c_double),
+        ("blocking_latency", C.c_double), ("tpot", C.c_double),
+        ("slo_violated", C.c_int), ("pad", C.c_int),
     ]
 
 
@@ -96,6 +108,50 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         )
     _lib = bind(C.CDLL(path))
     return _lib
+
+
+class ProbeRequest(C.Structure):
+    """pascal_probe_request (include/pascal_b200.h; RequestState,
+    proj/include/pascalsim/instance.hpp:41-62)."""
+
+    _fields_ = [
+        ("arrival_time", C.c_double),
+        ("prompt_tokens", C.c_long), ("reasoning_tokens", C.c_long),
+        ("answering_tokens", C.c_long),
+        ("phase", C.c_int), ("kv_location", C.c_int),
+        ("swapping_in", C.c_int), ("swapping_out", C.c_int),
+        ("tokens_generated", C.c_long), ("kv_tokens", C.c_long),
+        ("quantum_used_in_round", C.c_long), ("quanta_exhausted", C.c_long),
+        ("enqueue_seq", C.c_ulonglong),
+    ]
+
+
+class ProbeState(C.Structure):
+    """pascal_probe_state (include/pascal_b200.h)."""
+
+    _fields_ = [
+        ("requests", C.POINTER(ProbeRequest)), ("n_requests", C.c_long),
+        ("high_queue", C.POINTER(C.c_long)), ("n_high", C.c_long),
+        ("low_queue", C.POINTER(C.c_long)), ("n_low", C.c_long),
+        ("gpu_capacity", C.c_long), ("gpu_used", C.c_long), ("cpu_used", C.c_long),
+        ("enqueue_counter", C.c_ulonglong), ("demotion_threshold", C.c_long),
+        ("policy", C.c_char_p), ("now", C.c_double), ("candidate_scratch", C.c_int),
+    ]
+
+
+class ProbePlan(C.Structure):
+    """pascal_probe_plan (include/pascal_b200.h)."""
+
+    _LISTS = ("demoted", "evictions", "swap_ins", "immediate_swap_ins", "denied", "batch")
+    _fields_ = [
+        ("kind", C.c_int), ("over_capacity", C.c_int), ("prefill_request", C.c_long),
+        ("completion_time", C.c_double), ("gpu_used", C.c_long), ("cpu_used", C.c_long),
+    ] + [(k, C.POINTER(C.c_long)) for k in _LISTS] + [
+        ("n_" + k, C.c_long) for k in _LISTS] + [
+        ("swap_event_request", C.POINTER(C.c_long)),
+        ("swap_event_time", C.POINTER(C.c_double)), ("n_swap_events", C.c_long),
+        ("blocked", C.POINTER(C.c_double)),
+    ]
 
 
 def bind(lib: C.CDLL, extensions: bool = True) -> C.CDLL:
@@ -131,6 +187,7 @@ def bind(lib: C.CDLL, extensions: bool = True) -> C.CDLL:
         "pascal_batch_execute": (st, [P]),
         "pascal_batch_summaries": (st, [P, C.POINTER(Summary)]),
         "pascal_batch_free": (None, [P]),
+        "pascal_batch_rows": (st, [P, C.c_size_t, C.POINTER(RequestRow)]),
         "pascal_run_batch": (st, [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                   C.POINTER(RunConfig), C.c_size_t, C.POINTER(Summary)]),
         "pascal_last_timing": (st, [C.POINTER(Timing)]),
@@ -152,6 +209,10 @@ def bind(lib: C.CDLL, extensions: bool = True) -> C.CDLL:
         "pascal_batch_histograms": (st, [P, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
         "pascal_sweep": (st, [P, P, C.POINTER(RunConfig), C.POINTER(C.c_char_p), C.c_size_t,
                               C.POINTER(C.c_double), C.c_size_t, C.c_char_p]),
+        "pascal_probe_maybe_start": (st, [C.POINTER(ProbeState), P, C.POINTER(ProbePlan)]),
+        "pascal_probe_select": (st, [C.c_int, C.c_long, C.c_int, C.POINTER(C.c_ubyte),
+                                     C.POINTER(C.c_long), C.POINTER(C.c_long),
+                                     C.POINTER(C.c_int)]),
     }
     for name, (res, args) in sig.items():
         if not extensions and not hasattr(lib, name):

@@ -276,6 +276,13 @@ class Batch:
         _check(_lib_().pascal_batch_summaries(self._h, out))
         return list(out)
 
+    def rows(self, replica: int, n_requests: int) -> List[_lib.RequestRow]:
+        """Per-request TTFT / TTFAT / QoE / blocking / TPOT of one replica
+        (trace order), pascal_batch_rows."""
+        out = (_lib.RequestRow * max(n_requests, 1))()
+        _check(_lib_().pascal_batch_rows(self._h, replica, out))
+        return list(out)[:n_requests]
+
     def set_groups(self, group_of_replica: Sequence[int], n_groups: int) -> None:
         self.n_groups = n_groups
         arr = (C.c_int * self.n)(*group_of_replica)
@@ -320,3 +327,84 @@ def set_device(device: int) -> None:
 
 def device_available() -> bool:
     return bool(_lib_().pascal_device_available())
+
+
+# ---- unit-parity seams (pascal_probe_*; include/pascal_b200.h) -----------
+PHASES = {"waiting": 0, "reasoning": 1, "answering": 2, "done": 4}
+LOCATIONS = {"gpu": 0, "cpu": 1, "transit": 2}
+
+
+def probe_maybe_start(requests: Sequence[dict], high: Sequence[int], low: Sequence[int],
+                      gpu_capacity: int, gpu_used: int = 0, cpu_used: int = 0,
+                      policy: str = "pascal", profile: Optional[Profile] = None,
+                      enqueue_counter: int = 0, demotion_threshold: int = 5000,
+                      now: float = 0.0, candidate_scratch: int = 256) -> dict:
+    """One maybe_start step (apply_demotion + plan_iteration + plan application,
+    proj/src/engine.cpp:192-258) on a hand-built instance state, run by the
+    device engine's planner. `requests[k]` (id k) holds RequestState fields:
+    prompt/reasoning/answering, phase ("waiting"|"reasoning"|"answering"|
+    "done"), loc ("gpu"|"cpu"|"transit"), swapping_in/out, tokens, kv, qused,
+    quanta, seq, arrival (default k)."""
+    n = len(requests)
+    arr = (_lib.ProbeRequest * max(n, 1))()
+    for k, r in enumerate(requests):
+        a = arr[k]
+        a.arrival_time = float(r.get("arrival", k))
+        a.prompt_tokens = r.get("prompt", 1)
+        a.reasoning_tokens = r.get("reasoning", 0)
+        a.answering_tokens = r.get("answering", 1)
+        a.phase = PHASES[r.get("phase", "waiting")]
+        a.kv_location = LOCATIONS[r.get("loc", "gpu")]
+        a.swapping_in = int(bool(r.get("swapping_in", False)))
+        a.swapping_out = int(bool(r.get("swapping_out", False)))
+        a.tokens_generated = r.get("tokens", 0)
+        a.kv_tokens = r.get("kv", 0)
+        a.quantum_used_in_round = r.get("qused", 0)
+        a.quanta_exhausted = r.get("quanta", 0)
+        a.enqueue_seq = r.get("seq", 0)
+    hq = (C.c_long * max(len(high), 1))(*high)
+    lq = (C.c_long * max(len(low), 1))(*low)
+    st = _lib.ProbeState(arr, n, hq, len(high), lq, len(low), gpu_capacity, gpu_used, cpu_used,
+                         enqueue_counter, demotion_threshold, policy.encode(), float(now),
+                         candidate_scratch)
+    out = _lib.ProbePlan()
+    bufs = {}
+    for name in _lib.ProbePlan._LISTS + ("swap_event_request",):
+        bufs[name] = (C.c_long * max(n, 1))()
+        setattr(out, name, bufs[name])
+    times = (C.c_double * max(2 * n, 1))()
+    blocked = (C.c_double * max(n, 1))()
+    evreq = (C.c_long * max(2 * n, 1))()
+    out.swap_event_request = evreq
+    out.swap_event_time = times
+    out.blocked = blocked
+    prof = profile if profile is not None else Profile.default()
+    _check(_lib_().pascal_probe_maybe_start(C.byref(st), prof.handle, C.byref(out)))
+    res = {"kind": ("idle", "prefill", "decode")[out.kind],
+           "prefill_request": out.prefill_request, "completion_time": out.completion_time,
+           "gpu_used": out.gpu_used, "cpu_used": out.cpu_used,
+           "over_capacity": bool(out.over_capacity),
+           "swap_events": [(evreq[k], times[k]) for k in range(out.n_swap_events)],
+           "blocked": [blocked[k] for k in range(n)]}
+    for name in _lib.ProbePlan._LISTS:
+        res[name] = [bufs[name][k] for k in range(getattr(out, "n_" + name))]
+    return res
+
+
+def probe_select(mode: int, on_track, key1, key2=None):
+    """Alg. 1 (mode 0: select_instance_reasoning), Alg. 2 (mode 1:
+    select_instance_answering) or the baseline route (mode 2: argmin m_i) for
+    a batch of snapshot vectors, through the device engine's
+    select_instance. Arrays are (count, n): on_track t_i, key1 m_i or r_i,
+    key2 a_i. Returns the chosen instance per vector (numpy int32)."""
+    import numpy as np
+    t = np.ascontiguousarray(on_track, dtype=np.uint8)
+    count, n = t.shape
+    k1 = np.ascontiguousarray(key1, dtype=np.int64)
+    k2 = np.ascontiguousarray(key2 if key2 is not None else np.zeros_like(k1), dtype=np.int64)
+    out = np.zeros(count, dtype=np.int32)
+    _check(_lib_().pascal_probe_select(
+        mode, count, n, t.ctypes.data_as(C.POINTER(C.c_ubyte)),
+        k1.ctypes.data_as(C.POINTER(C.c_long)), k2.ctypes.data_as(C.POINTER(C.c_long)),
+        out.ctypes.data_as(C.POINTER(C.c_int))))
+    return out

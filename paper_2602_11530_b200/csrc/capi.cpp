@@ -19,6 +19,13 @@
 
 using namespace pbh;
 
+namespace pbh {  // host/probe.cpp
+void probe_maybe_start(const pascal_probe_state& st, const pb::Profile& prof,
+                       pascal_probe_plan& out);
+void probe_select(int mode, long count, int n, const unsigned char* t, const long* k1,
+                  const long* k2, int* out);
+}  // namespace pbh
+
 namespace {
 
 thread_local std::string g_err;
@@ -353,6 +360,20 @@ pascal_status pascal_batch_summaries(pascal_batch* b, pascal_summary* out) {
     });
 }
 
+pascal_status pascal_batch_rows(pascal_batch* b, size_t replica, pascal_request_row* out) {
+    return guarded([&] {
+        need(b && b->b && out, "null argument");
+        std::vector<std::vector<Row>> rows;
+        batch_rows(b->b, rows);
+        need(replica < rows.size(), "replica out of range");
+        for (size_t k = 0; k < rows[replica].size(); ++k) {
+            const Row& w = rows[replica][k];
+            out[k] = pascal_request_row{w.id, w.ttft, w.ttfat, w.qoe, w.blocking, w.tpot,
+                                        w.slo ? 1 : 0, 0};
+        }
+    });
+}
+
 void pascal_batch_free(pascal_batch* b) {
     if (!b) return;
     batch_free(b->b);
@@ -564,6 +585,20 @@ pascal_status pascal_trace_get(const pascal_trace* t, long i, long* id, double* 
 
 long long pascal_trace_request_iterations(const pascal_trace* t) {
     return t ? request_iterations(t->t) : 0;
+}
+
+pascal_status pascal_probe_maybe_start(const pascal_probe_state* st, const pascal_profile* p,
+                                       pascal_probe_plan* out) {
+    return guarded([&] {
+        need(st && p && out, "null argument");
+        check_profile(p->p);
+        probe_maybe_start(*st, p->p, *out);
+    });
+}
+
+pascal_status pascal_probe_select(int mode, long count, int n, const unsigned char* on_track,
+                                  const long* key1, const long* key2, int* out) {
+    return guarded([&] { probe_select(mode, count, n, on_track, key1, key2, out); });
 }
 
 pascal_status pascal_set_device(int device) {

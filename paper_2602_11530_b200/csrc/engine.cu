@@ -2026,6 +2026,195 @@ int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slot
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
+#if PB_LOG
+// ---------------------------------------------------- unit-parity seams
+// One maybe_start (demotion + plan_iteration + plan application,
+// engine.cpp:192-258 / instance.cpp:39-57,103-282) on a hand-built instance
+// state, through the same inlined planner the event loop runs. One warp.
+__global__ void __launch_bounds__(32, 1) plan_probe_kernel(PlanProbe p) {
+    extern __shared__ __align__(16) char smem_raw[];
+    Rep R;
+    R.n = p.n;
+    R.ni = p.ni;
+    R.policy = p.policy;
+    R.flags = kLogEvents;
+    R.cap = p.cap;
+    R.quantum = p.quantum;
+    R.demotion = p.demotion;
+    R.slack = 0;
+    R.tpot = 0.1;
+    R.prof = p.prof;
+    R.logcap = p.log_cap;
+    R.arrival = p.arrival;
+    R.spec = p.spec;
+    R.aoff = p.aoff;
+    R.rs = p.rs;
+    R.blocked = p.blocked;
+    R.rec = p.rec;
+    R.ph = p.ph;
+    R.bpv = nullptr;
+    R.bpk = nullptr;
+    R.dig = nullptr;
+    R.del = nullptr;
+    R.qent = p.qent;
+    R.qcap = p.qcap;
+    R.batch = p.batch;
+    R.heap = p.heap;
+    R.g_cand = p.cand;
+    R.g_tmp = p.tmp;
+    R.g_tmpq = p.tmpq;
+    R.g_cstat = p.cstat;
+    R.elist = p.elist;
+    R.stack = p.stack;
+    R.log = p.log;
+    const int ni = p.ni;
+    char* sp = smem_raw;
+    R.s.gpu = reinterpret_cast<long long*>(sp);
+    R.s.cpu = R.s.gpu + ni;
+    R.s.iter_start = reinterpret_cast<double*>(R.s.cpu + ni);
+    R.s.link = R.s.iter_start + ni;
+    R.s.hi_len = reinterpret_cast<int*>(R.s.link + ni);
+    R.s.lo_len = R.s.hi_len + ni;
+    R.s.hcount = R.s.lo_len + ni;
+    R.s.lcount = R.s.hcount + ni;
+    R.s.afresh = R.s.lcount + ni;
+    R.s.blen = R.s.afresh + ni;
+    R.s.busy = R.s.blen + ni;
+    R.s.healthy = R.s.busy + ni;
+    sp += smem_inst_bytes(ni);
+    R.c_smem = p.c_smem;
+    R.s_cand = reinterpret_cast<int4*>(sp);
+    R.s_tmp = R.s_cand + p.c_smem;
+    R.s_tmpq = reinterpret_cast<unsigned*>(R.s_tmp + p.c_smem);
+    R.s_cstat = reinterpret_cast<unsigned char*>(R.s_tmpq + p.c_smem);
+    for (int i = lane_id(); i < ni; i += 32) {
+        R.s.gpu[i] = p.used[2 * i];
+        R.s.cpu[i] = p.used[2 * i + 1];
+        R.s.iter_start[i] = 0.0;
+        R.s.link[i] = 0.0;
+        R.s.hi_len[i] = p.qlen[2 * i];
+        R.s.lo_len[i] = p.qlen[2 * i + 1];
+        // monitor counters r_i, |low|, a_i of the live entries
+        int hc = 0, lc = 0, af = 0;
+        for (int k = 0; k < p.qlen[2 * i]; ++k) hc += 1;
+        const uint2* lq = p.qent + (long long)(2 * i + 1) * p.qcap;
+        for (int k = 0; k < p.qlen[2 * i + 1]; ++k) {
+            lc += 1;
+            af += p.rs[lq[k].x].h.w == 0;
+        }
+        R.s.hcount[i] = hc;
+        R.s.lcount[i] = lc;
+        R.s.afresh[i] = af;
+        R.s.blen[i] = 0;
+        R.s.busy[i] = 0;
+        R.s.healthy[i] = 1;
+    }
+    __syncwarp();
+    Scal S;
+    S.heap = p.heap;
+    S.heap_slots = p.heap_cap;
+    S.now = p.now;
+    S.evseq = 0;
+    S.enq = p.enq;
+    S.next_arr = p.n;
+    S.hn = 0;
+    S.done = 0;
+    S.status = 0;
+    long long tot = 0;
+    for (int i = 0; i < ni; ++i) tot += p.used[2 * i];
+    S.gpu_total = tot;
+    S.peak = tot;
+    S.nlog = 0;
+    S.events = S.plans = S.visits = S.req_iters = S.ans_tokens = S.health = 0;
+    S.adm_rounds = S.adm_slow = 0;
+    maybe_start<false>(R, S, p.inst);
+    __syncwarp();
+    if (lane_id() == 0) {
+        for (int i = 0; i < ni; ++i) {
+            p.out_used[2 * i] = R.s.gpu[i];
+            p.out_used[2 * i + 1] = R.s.cpu[i];
+        }
+        p.out_scal[0] = S.status;
+        p.out_scal[1] = S.hn;
+        p.out_scal[2] = (int)S.nlog;
+        p.out_scal[3] = R.s.blen[p.inst];
+        p.out_scal[4] = R.s.busy[p.inst];
+    }
+}
+
+int launch_plan_probe(const PlanProbe& p, void* stream) {
+    const size_t smem = (size_t)smem_inst_bytes(p.ni) + smem_cand_bytes(p.c_smem);
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(plan_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return 2;
+    plan_probe_kernel<<<1, 32, smem, (cudaStream_t)stream>>>(p);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+// Alg. 1 / Alg. 2 placement (cluster.cpp:10-44,59-62) for a batch of
+// snapshot vectors through the engine's select_instance: one warp per
+// vector; instance i's m_i / r_i / a_i go to the counters select_instance
+// reads, and t_i = 0 is realised as one behind-schedule answering request in
+// the instance's low queue (the health scan's own input), t_i = 1 as an empty
+// low queue.
+constexpr int kSelProbeMaxN = 32;
+constexpr int kSelProbeWarps = 4;
+__global__ void __launch_bounds__(kSelProbeWarps * 32) select_probe_kernel(SelectProbe p) {
+    struct W {
+        long long gpu[kSelProbeMaxN], cpu[kSelProbeMaxN];
+        int hcount[kSelProbeMaxN], afresh[kSelProbeMaxN], lo_len[kSelProbeMaxN];
+        uint2 qent[2 * kSelProbeMaxN];
+        unsigned rejected[kSelProbeMaxN / 32 + 1];
+    };
+    __shared__ W ws[kSelProbeWarps];
+    W& w = ws[threadIdx.x >> 5];
+    const int n = p.n;
+    const long long nw = (long long)gridDim.x * kSelProbeWarps;
+    for (long long v = (long long)blockIdx.x * kSelProbeWarps + (threadIdx.x >> 5); v < p.count;
+         v += nw) {
+        __syncwarp();
+        for (int i = lane_id(); i < n; i += 32) {
+            const long long o = v * n + i;
+            const bool ok = p.t[o] != 0;
+            w.gpu[i] = p.mode == 1 ? 0 : p.k1[o];
+            w.cpu[i] = 0;
+            w.hcount[i] = p.mode == 1 ? (int)p.k1[o] : 0;
+            w.afresh[i] = p.mode == 1 ? (int)p.k2[o] : 0;
+            w.lo_len[i] = ok ? 0 : 1;
+            w.qent[2 * i] = make_uint2(0, 0);
+            w.qent[2 * i + 1] = make_uint2(0u, 1u);  // request 0, its live seq
+        }
+        __syncwarp();
+        HealthView V;
+        V.qent = w.qent;
+        V.qcap = 1;
+        V.lo_len = w.lo_len;
+        V.rs = p.rs;
+        V.spec = p.spec;
+        V.ph = p.ph;
+        V.bpk = p.bpk;
+        V.bpv = p.bpv;
+        V.aoff = p.aoff;
+        V.tpot = 1.0;
+        V.slack = 0;
+        V.ni = n;
+        const int mode = p.mode == 0 ? SEL_M_HEALTHY : p.mode == 1 ? SEL_ANSWER : SEL_M;
+        const SelOut o = select_instance(V, 100.0, mode, w.gpu, w.cpu, w.hcount, w.afresh,
+                                         w.rejected);
+        if (lane_id() == 0) p.out[v] = o.id;
+    }
+}
+
+int launch_select_probe(const SelectProbe& p, void* stream) {
+    if (p.n < 1 || p.n > kSelProbeMaxN) return 1;
+    const long long want = (p.count + kSelProbeWarps - 1) / kSelProbeWarps;
+    const int blocks = (int)(want < 4096 ? (want > 0 ? want : 1) : 4096);
+    select_probe_kernel<<<blocks, kSelProbeWarps * 32, 0, (cudaStream_t)stream>>>(p);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+#endif  // PB_LOG
+
 #endif  // !PB_PDES
 
 #if PB_PDES

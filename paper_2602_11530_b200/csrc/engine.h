@@ -187,6 +187,8 @@ struct DevSummary {
     long long slo_violations;
     long long adm_rounds, adm_slow;
     int status, pad;
+    double tpot_mean;        // over requests with A > 1
+    long long tpot_requests;
 };
 
 // Per-request metric outputs (trace order), proj/include/pascalsim/metrics.hpp:58-67.
@@ -197,6 +199,7 @@ struct RowArrays {
     double* blocking;
     unsigned char* slo;
     double* ttft_sorted;
+    double* tpot;  // (completion - first answer delivery) / (A - 1); 0 when A <= 1
 };
 
 #ifdef __CUDACC__
@@ -254,6 +257,62 @@ PB_HD inline int pdes_smem(int ni, int hs, int c_smem, int warps) {
     return pdes_inst_bytes(ni, hs) + warps * pdes_warp_bytes(c_smem) + pdes_ctl_bytes();
 }
 
+// Unit-parity seams (pascal_probe_* in include/pascal_b200.h): one
+// maybe_start on a hand-built instance state, run by the logging build's own
+// planner (one warp). The host fills the request / queue / instance arrays in
+// the engine's layout; the outputs are the decision log, the heap (pushed
+// events), the batch list and the instance counters.
+struct PlanProbe {
+    int n, ni, inst, policy;
+    long long cap, quantum, demotion;
+    double now;
+    Profile prof;
+    unsigned enq;  // enqueue seqs handed out so far (demotions take the next ones)
+    int c_smem;    // shared-memory candidate slots
+    ReqState* rs;
+    int4* spec;
+    double* arrival;
+    double* blocked;
+    RecOut* rec;
+    PacerHot* ph;
+    int* aoff;
+    uint2* qent;  // 2 * ni queues of qcap entries
+    long long qcap;
+    const int* qlen;         // [2 * ni] {high, low} live lengths
+    const long long* used;   // [2 * ni] {gpu_used, cpu_used}
+    unsigned* batch;         // ni * n
+    HeapEnt* heap;           // heap_cap slots (1-based)
+    long long heap_cap;
+    LogEnt* log;
+    long long log_cap;
+    int4* cand;
+    int4* tmp;
+    unsigned* tmpq;
+    unsigned char* cstat;
+    unsigned* elist;
+    unsigned* stack;
+    long long* out_used;     // [2 * ni] after the step
+    int* out_scal;           // {status, heap entries, log entries, batch length, busy}
+};
+// Batched Alg. 1 / Alg. 2 evaluation through the engine's select_instance:
+// vector v has n instances with on-track flags t[v*n+i] and keys k1 (m_i for
+// modes 0 / 2, r_i for mode 1) and k2 (a_i, mode 1).
+struct SelectProbe {
+    int mode;  // 0 select_instance_reasoning, 1 select_instance_answering, 2 argmin m_i
+    int n;
+    long long count;
+    const unsigned char* t;
+    const long long* k1;
+    const long long* k2;
+    int* out;
+    ReqState* rs;  // one behind-schedule answering request (the unhealthy member)
+    int4* spec;
+    PacerHot* ph;
+    int* aoff;
+    int* bpk;
+    double* bpv;
+};
+
 constexpr int kHistBins = 128;  // PASCAL_HIST_BINS
 
 // Host entries (engine.cu / metrics.cu). All enqueue on `stream`.
@@ -263,6 +322,8 @@ constexpr int kHistBins = 128;  // PASCAL_HIST_BINS
 namespace logging {
 int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,
                   int warps_per_block, int blocks, void* stream);
+int launch_plan_probe(const PlanProbe& p, void* stream);
+int launch_select_probe(const SelectProbe& p, void* stream);
 }
 namespace nolog {
 int launch_engine(const Arena& a, int max_ni, int n_smem, int c_smem, int h_slots, int b_smem,

@@ -99,6 +99,7 @@ struct Row {  // proj/include/pascalsim/metrics.hpp:58-67
     double ttft = 0, ttfat = 0, qoe = 0;
     bool slo = false;
     double blocking = 0;
+    double tpot = 0;  // device-only output (not written to requests.csv)
 };
 struct Bin {
     long lo = 0, hi = 0, count = 0;
@@ -125,6 +126,8 @@ struct DeviceSummary {  // mirrors pascal_summary
     long long slo_violations;
     long long adm_rounds, adm_slow;
     int status, pad;
+    double tpot_mean;
+    long long tpot_requests;
 };
 
 struct Job {

@@ -339,7 +339,7 @@ public:
     DevBuf<unsigned char> d_cstat_, d_slo_;
     DevBuf<pb::LogEnt> d_log_;
     DevBuf<pb::MetricParams> d_params_;
-    DevBuf<double> d_ttft_, d_ttfat_, d_qoe_, d_block_, d_sorted_;
+    DevBuf<double> d_ttft_, d_ttfat_, d_qoe_, d_block_, d_sorted_, d_tpot_;
     DevBuf<pb::DevSummary> d_sum_;
     DevBuf<char> d_sort_tmp_;
     size_t sort_bytes_ = 0;
@@ -588,6 +588,7 @@ void Batch::build() {
     d_echo_.ensure(n_rep_);
     d_seg_.ensure(n_rep_ + 1);
     d_ttft_.ensure(rq);
+    d_tpot_.ensure(rq);
     d_ttfat_.ensure(rq);
     d_qoe_.ensure(rq);
     d_block_.ensure(rq);
@@ -595,7 +596,8 @@ void Batch::build() {
     d_sorted_.ensure(rq);
     d_sum_.ensure(n_rep_);
 
-    pb::RowArrays rows{d_ttft_.p, d_ttfat_.p, d_qoe_.p, d_block_.p, d_slo_.p, d_sorted_.p};
+    pb::RowArrays rows{d_ttft_.p, d_ttfat_.p, d_qoe_.p, d_block_.p, d_slo_.p, d_sorted_.p,
+                       d_tpot_.p};
     pb::Arena ar = arena(false);
     size_t bytes = 0;
     if (pb::launch_metrics(ar, d_params_.p, d_seg_.p, d_rid_.p, rq, n_rep_, rows, d_sum_.p,
@@ -804,7 +806,8 @@ void Batch::execute() {
     pb::Arena pa = arena(false);
     run(false);
     ck(cudaEventRecord(ev_[2], st_), "event");
-    pb::RowArrays rows{d_ttft_.p, d_ttfat_.p, d_qoe_.p, d_block_.p, d_slo_.p, d_sorted_.p};
+    pb::RowArrays rows{d_ttft_.p, d_ttfat_.p, d_qoe_.p, d_block_.p, d_slo_.p, d_sorted_.p,
+                       d_tpot_.p};
     size_t bytes = sort_bytes_;
     if (pb::launch_metrics(pa, d_params_.p, d_seg_.p, d_rid_.p, total_req_, n_rep_, rows,
                            d_sum_.p, d_echo_.p, d_sort_tmp_.p, &bytes, st_) != 0)
@@ -855,7 +858,7 @@ void Batch::fetch_single(RunOutputs& o, bool records, bool log) {
     o.status = s[0].status;
     o.capacity = s[0].capacity;
     const long long n = total_req_;
-    std::vector<double> ttft(n), ttfat(n), qoe(n), blk(n);
+    std::vector<double> ttft(n), ttfat(n), qoe(n), blk(n), tpot(n);
     std::vector<unsigned char> slo(n);
     auto down = [&](void* dst, const void* src, size_t b) {
         if (b) ck(cudaMemcpy(dst, src, b, cudaMemcpyDeviceToHost), "d2h");
@@ -864,6 +867,7 @@ void Batch::fetch_single(RunOutputs& o, bool records, bool log) {
     down(ttfat.data(), d_ttfat_.p, n * sizeof(double));
     down(qoe.data(), d_qoe_.p, n * sizeof(double));
     down(blk.data(), d_block_.p, n * sizeof(double));
+    down(tpot.data(), d_tpot_.p, n * sizeof(double));
     down(slo.data(), d_slo_.p, n);
     const Trace& t = *jobs_[0].trace;
     o.rows.resize(n);
@@ -877,6 +881,7 @@ void Batch::fetch_single(RunOutputs& o, bool records, bool log) {
         w.qoe = qoe[k];
         w.slo = slo[k] != 0;
         w.blocking = blk[k];
+        w.tpot = tpot[k];
     }
     if (records) {
         o.rec.resize(n);
@@ -908,7 +913,7 @@ void Batch::fetch_single(RunOutputs& o, bool records, bool log) {
 void Batch::fetch_rows(std::vector<std::vector<Row>>& rows) {
     ScopedDevice sd(dev_);
     const long long n = total_req_;
-    std::vector<double> ttft(n), ttfat(n), qoe(n), blk(n);
+    std::vector<double> ttft(n), ttfat(n), qoe(n), blk(n), tpot(n);
     std::vector<unsigned char> slo(n);
     auto down = [&](void* dst, const void* src, size_t b) {
         if (b) ck(cudaMemcpy(dst, src, b, cudaMemcpyDeviceToHost), "d2h");
@@ -917,6 +922,7 @@ void Batch::fetch_rows(std::vector<std::vector<Row>>& rows) {
     down(ttfat.data(), d_ttfat_.p, n * sizeof(double));
     down(qoe.data(), d_qoe_.p, n * sizeof(double));
     down(blk.data(), d_block_.p, n * sizeof(double));
+    down(tpot.data(), d_tpot_.p, n * sizeof(double));
     down(slo.data(), d_slo_.p, n);
     rows.assign(n_rep_, {});
     long long g = 0;
@@ -933,6 +939,7 @@ void Batch::fetch_rows(std::vector<std::vector<Row>>& rows) {
             w.qoe = qoe[g];
             w.slo = slo[g] != 0;
             w.blocking = blk[g];
+            w.tpot = tpot[g];
         }
     }
 }

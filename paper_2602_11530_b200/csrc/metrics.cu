@@ -97,6 +97,13 @@ __global__ void rows_kernel(const int* rid, const MetricParams* params, const in
     rows.qoe[g] = q;
     rows.blocking[g] = blk;
     rows.slo[g] = q < mp.qoe_threshold ? 1 : 0;
+    // per-request TPOT (not a reference output): the answer
+    // tokens after the first are delivered over [first delivery, completion]
+    // (the last token is delivered at the finishing iteration's end,
+    // engine.cpp:320-337)
+    rows.tpot[g] = sp.z > 1 ? __ddiv_rn(__dsub_rn(r.completion, r.first_answer_delivery),
+                                        (double)(sp.z - 1))
+                            : 0.0;
 }
 
 __device__ __forceinline__ double nearest_rank(const double* v, long long n, double pct) {
@@ -132,8 +139,11 @@ __global__ void summary_kernel(const MetricParams* params, const ReplicaDesc* de
     s.adm_slow = o.adm_slow;
     s.status = o.status;
     s.pad = 0;
+    s.tpot_mean = 0.0;
+    s.tpot_requests = 0;
     if (o.status == 0 && n > 0) {
-        long long viol = 0, ok = 0, tokens = 0;
+        long long viol = 0, ok = 0, tokens = 0, ntp = 0;
+        double tsum = 0.0;
         double first = rec[base].arrival, last = rec[base].completion;
         for (long long k = lane; k < n; k += 32) {
             long long g = base + k;
@@ -141,6 +151,10 @@ __global__ void summary_kernel(const MetricParams* params, const ReplicaDesc* de
             ok += rows.ttfat[g] <= mp.ttfat_target ? 1 : 0;
             int4 sp = spec[g];
             tokens += (long long)sp.y + sp.z;
+            if (sp.z > 1) {
+                tsum = __dadd_rn(tsum, rows.tpot[g]);
+                ++ntp;
+            }
             double a = rec[g].arrival, c = rec[g].completion;
             first = a < first ? a : first;
             last = last < c ? c : last;
@@ -149,6 +163,8 @@ __global__ void summary_kernel(const MetricParams* params, const ReplicaDesc* de
             viol += __shfl_xor_sync(FULLM, viol, off);
             ok += __shfl_xor_sync(FULLM, ok, off);
             tokens += __shfl_xor_sync(FULLM, tokens, off);
+            ntp += __shfl_xor_sync(FULLM, ntp, off);
+            tsum = __dadd_rn(tsum, __shfl_xor_sync(FULLM, tsum, off));
             double f2 = __shfl_xor_sync(FULLM, first, off);
             double l2 = __shfl_xor_sync(FULLM, last, off);
             first = f2 < first ? f2 : first;
@@ -169,6 +185,8 @@ __global__ void summary_kernel(const MetricParams* params, const ReplicaDesc* de
             s.slo_violations = viol;
             double span = __dsub_rn(last, first);
             s.throughput = span <= 0.0 ? 0.0 : __ddiv_rn((double)tokens, span);
+            s.tpot_requests = ntp;
+            s.tpot_mean = ntp > 0 ? __ddiv_rn(tsum, (double)ntp) : 0.0;
         }
     }
     if (lane == 0) sum[r] = s;
