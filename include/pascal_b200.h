@@ -100,6 +100,20 @@ pascal_status pascal_run_batch(const pascal_trace* const* traces,
 
 pascal_status pascal_last_timing(pascal_timing* out);
 
+/* ---- Several GPUs of one process (replicas shard, no
+ * data-path collective). Replicas are split into cost-balanced parts
+ * (longest-first greedy over predicted work = request-iterations x a
+ * per-policy factor, ties to the lowest part; deterministic), one part per
+ * listed device, each run as one device batch by its own host thread.
+ * devices = NULL / n_devices = 0: the current device only. */
+pascal_status pascal_partition_replicas(const pascal_trace* const* traces,
+                                        const pascal_run_config* cfgs, size_t count, int n_parts,
+                                        int* part_of_replica);
+pascal_status pascal_run_batch_devices(const pascal_trace* const* traces,
+                                       const pascal_profile* const* profiles,
+                                       const pascal_run_config* cfgs, size_t count,
+                                       const int* devices, int n_devices, pascal_summary* out);
+
 /* The reference CLI's `pascalsim sweep` (proj/tools/pascalsim_cli.cpp:
  * 299-342) as one device batch: every (policy, capacity fraction) point of
  * the grid is simulated side by side, then <out_dir>/<policy>_f<%.2f>.{
@@ -110,6 +124,12 @@ pascal_status pascal_sweep(const pascal_trace* t, const pascal_profile* p,
                            const pascal_run_config* base, const char* const* policies,
                            size_t n_policies, const double* fractions, size_t n_fractions,
                            const char* out_dir);
+/* pascal_sweep with the grid points spread over `devices` (as above);
+ * outputs are identical for any device list. */
+pascal_status pascal_sweep_devices(const pascal_trace* t, const pascal_profile* p,
+                                   const pascal_run_config* base, const char* const* policies,
+                                   size_t n_policies, const double* fractions, size_t n_fractions,
+                                   const char* out_dir, const int* devices, int n_devices);
 
 /* Parity: per-request records in the hex-float dump format of
  * oracle/ref_dump.cpp (id order) and, when event_log_path is non-NULL, the

@@ -31,6 +31,7 @@ ABI_SYMBOLS = (
     "pascal_batch_histograms",
     "pascal_sweep",
     "pascal_probe_maybe_start", "pascal_probe_select", "pascal_batch_rows",
+    "pascal_partition_replicas", "pascal_run_batch_devices", "pascal_sweep_devices",
 )
 HIST_BINS = 128
 
@@ -188,6 +189,14 @@ def bind(lib: C.CDLL, extensions: bool = True) -> C.CDLL:
         "pascal_batch_summaries": (st, [P, C.POINTER(Summary)]),
         "pascal_batch_free": (None, [P]),
         "pascal_batch_rows": (st, [P, C.c_size_t, C.POINTER(RequestRow)]),
+        "pascal_partition_replicas": (st, [C.POINTER(C.c_void_p), C.POINTER(RunConfig),
+                                           C.c_size_t, C.c_int, C.POINTER(C.c_int)]),
+        "pascal_run_batch_devices": (st, [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                          C.POINTER(RunConfig), C.c_size_t,
+                                          C.POINTER(C.c_int), C.c_int, C.POINTER(Summary)]),
+        "pascal_sweep_devices": (st, [P, P, C.POINTER(RunConfig), C.POINTER(C.c_char_p),
+                                      C.c_size_t, C.POINTER(C.c_double), C.c_size_t, C.c_char_p,
+                                      C.POINTER(C.c_int), C.c_int]),
         "pascal_run_batch": (st, [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                   C.POINTER(RunConfig), C.c_size_t, C.POINTER(Summary)]),
         "pascal_last_timing": (st, [C.POINTER(Timing)]),

@@ -305,14 +305,38 @@ def run_batch(traces, profiles, cfgs) -> List[_lib.Summary]:
     return list(out)
 
 
+def run_batch_devices(traces, profiles, cfgs, devices: Sequence[int]) -> List[_lib.Summary]:
+    """pascal_run_batch over several GPUs of this process (cost-balanced
+    replica parts, one host thread per device)."""
+    n, tt, pp, cc = _arrays(traces, profiles, cfgs)
+    out = (_lib.Summary * n)()
+    dv = (C.c_int * max(len(devices), 1))(*devices)
+    _check(_lib_().pascal_run_batch_devices(tt, pp, cc, n, dv, len(devices), out))
+    return list(out)
+
+
+def partition_replicas(traces, cfgs, n_parts: int) -> List[int]:
+    """pascal_partition_replicas: the device part of every replica (host-only)."""
+    n = len(traces)
+    tt = (C.c_void_p * n)(*[t.handle.value for t in traces])
+    cc = (_lib.RunConfig * n)(*cfgs)
+    out = (C.c_int * max(n, 1))()
+    _check(_lib_().pascal_partition_replicas(tt, cc, n, n_parts, out))
+    return list(out)[:n]
+
+
 def run_sweep(trace: Trace, profile: Profile, base_cfg, policies: Sequence[str],
-          fractions: Sequence[float], out_dir: str) -> None:
-    """`pascalsim sweep` (proj/tools/pascalsim_cli.cpp:299-342) as one device
-    batch: per-point reports <out_dir>/<policy>_f<frac>.* and sweep.csv."""
+              fractions: Sequence[float], out_dir: str,
+              devices: Optional[Sequence[int]] = None) -> None:
+    """`pascalsim sweep` (proj/tools/pascalsim_cli.cpp:299-342) as device
+    batches: per-point reports <out_dir>/<policy>_f<frac>.* and sweep.csv;
+    `devices` spreads the grid over several GPUs."""
     pols = (C.c_char_p * len(policies))(*[_b(x) for x in policies])
     fr = (C.c_double * len(fractions))(*fractions)
-    _check(_lib_().pascal_sweep(trace.handle, profile.handle, C.byref(base_cfg), pols,
-                                len(policies), fr, len(fractions), _b(out_dir)))
+    dv = (C.c_int * max(len(devices or []), 1))(*(devices or []))
+    _check(_lib_().pascal_sweep_devices(trace.handle, profile.handle, C.byref(base_cfg), pols,
+                                        len(policies), fr, len(fractions), _b(out_dir), dv,
+                                        len(devices or [])))
 
 
 def last_timing() -> _lib.Timing:

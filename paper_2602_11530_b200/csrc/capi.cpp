@@ -5,12 +5,16 @@
 // std::exception -> 3; success clears the thread-local message; NULL handles
 // -> 1 "null argument"; *_free, pascal_trace_size and pascal_run_config_init
 // are unguarded. pascal_run drives the sm_100a engine (engine_host.cpp).
+#include <cuda_runtime.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <filesystem>
 #include <memory>
 #include <numeric>
+#include <exception>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pascal.h"
@@ -68,6 +72,100 @@ RunCfg to_cfg(const pascal_run_config* c) {
     r.qoe_threshold = c->qoe_threshold;
     r.slack = c->pacer_slack_tokens;
     return r;
+}
+
+// Predicted device work of a replica: its request-iterations (policy- and
+// rate-independent) times a per-policy factor (the Pascal /
+// RR planners scan, partition and preempt; FCFS and the oracle admit in
+// order), plus one oracle pass when the capacity is derived.
+double replica_cost(const Job& j) {
+    const double t = (double)request_iterations(*j.trace) + (double)j.trace->size();
+    double f = j.cfg.policy == pb::kPascal ? 4.0 : j.cfg.policy == pb::kRr ? 3.0 : 1.0;
+    if (j.cfg.gpu_capacity <= 0 && j.cfg.policy != pb::kOracle) f += 1.0;
+    return t * f;
+}
+
+// Longest-processing-time-first: replicas in descending predicted cost (ties
+// by index) each go to the currently least-loaded part (ties to the lowest
+// part index). Deterministic.
+std::vector<int> partition_lpt(const std::vector<Job>& jobs, int parts) {
+    std::vector<int> part(jobs.size(), 0);
+    if (parts <= 1) return part;
+    std::vector<double> cost(jobs.size());
+    for (size_t k = 0; k < jobs.size(); ++k) cost[k] = replica_cost(jobs[k]);
+    std::vector<size_t> ord(jobs.size());
+    std::iota(ord.begin(), ord.end(), size_t{0});
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return cost[a] > cost[b]; });
+    std::vector<double> load(parts, 0.0);
+    for (size_t k : ord) {
+        int best = 0;
+        for (int p = 1; p < parts; ++p)
+            if (load[p] < load[best]) best = p;
+        part[k] = best;
+        load[best] += cost[k];
+    }
+    return part;
+}
+
+// Simulates `jobs` over `devices` (one host thread per device, each running
+// one device batch of its part), results in input order.
+void run_jobs_devices(const std::vector<Job>& jobs, const std::vector<int>& devices,
+                      std::vector<DeviceSummary>& sum, std::vector<std::vector<Row>>* rows) {
+    if (!device_available()) throw std::logic_error("no CUDA device available for the B200 engine");
+    const int nd = (int)devices.size();
+    const std::vector<int> part = partition_lpt(jobs, nd);
+    sum.assign(jobs.size(), DeviceSummary{});
+    if (rows) rows->assign(jobs.size(), {});
+    std::vector<std::exception_ptr> err(nd);
+    auto work = [&](int d) {
+        try {
+            std::vector<size_t> idx;
+            std::vector<Job> sub;
+            for (size_t k = 0; k < jobs.size(); ++k)
+                if (part[k] == d) idx.push_back(k), sub.push_back(jobs[k]);
+            if (sub.empty()) return;
+            set_device(devices[d]);
+            std::unique_ptr<Batch, void (*)(Batch*)> b(batch_create(sub), batch_free);
+            batch_execute(b.get());
+            std::vector<DeviceSummary> s;
+            batch_summaries(b.get(), s);
+            std::vector<std::vector<Row>> r;
+            if (rows) batch_rows(b.get(), r);
+            for (size_t q = 0; q < idx.size(); ++q) {
+                sum[idx[q]] = s[q];
+                if (rows) (*rows)[idx[q]] = std::move(r[q]);
+            }
+        } catch (...) {
+            err[d] = std::current_exception();
+        }
+    };
+    if (nd == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> th;
+        for (int d = 0; d < nd; ++d) th.emplace_back(work, d);
+        for (auto& x : th) x.join();
+    }
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+}
+
+std::vector<int> device_list(const int* devices, int n_devices) {
+    std::vector<int> d;
+    if (devices == nullptr || n_devices <= 0) {
+        int cur = 0;
+        if (cudaGetDevice(&cur) != cudaSuccess) cur = 0;
+        d.push_back(cur);
+        return d;
+    }
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) count = 0;
+    for (int k = 0; k < n_devices; ++k) {
+        need(devices[k] >= 0 && devices[k] < count, "device index out of range");
+        for (int x : d) need(x != devices[k], "device listed twice");
+        d.push_back(devices[k]);
+    }
+    return d;
 }
 
 const char* kKindName[] = {"arrival",       "demote",           "evict",        "swap_in",
@@ -411,10 +509,54 @@ pascal_status pascal_run_batch(const pascal_trace* const* traces,
     return st;
 }
 
+pascal_status pascal_partition_replicas(const pascal_trace* const* traces,
+                                        const pascal_run_config* cfgs, size_t count, int n_parts,
+                                        int* part_of_replica) {
+    return guarded([&] {
+        need(traces && cfgs && part_of_replica, "null argument");
+        need(n_parts >= 1, "n_parts must be >= 1");
+        std::vector<Job> jobs(count);
+        for (size_t k = 0; k < count; ++k) {
+            need(traces[k] != nullptr, "null argument");
+            jobs[k] = Job{&traces[k]->t, to_cfg(&cfgs[k]), pb::Profile{}};
+        }
+        const std::vector<int> part = partition_lpt(jobs, n_parts);
+        std::copy(part.begin(), part.end(), part_of_replica);
+    });
+}
+
+pascal_status pascal_run_batch_devices(const pascal_trace* const* traces,
+                                       const pascal_profile* const* profiles,
+                                       const pascal_run_config* cfgs, size_t count,
+                                       const int* devices, int n_devices, pascal_summary* out) {
+    return guarded([&] {
+        need(traces && profiles && cfgs && out, "null argument");
+        std::vector<Job> jobs(count);
+        for (size_t k = 0; k < count; ++k) {
+            need(traces[k] && profiles[k], "null argument");
+            check_trace(traces[k]->t);
+            check_profile(profiles[k]->p);
+            jobs[k] = Job{&traces[k]->t, to_cfg(&cfgs[k]), profiles[k]->p};
+        }
+        std::vector<DeviceSummary> sum;
+        run_jobs_devices(jobs, device_list(devices, n_devices), sum, nullptr);
+        static_assert(sizeof(pascal_summary) == sizeof(DeviceSummary), "summary layout");
+        std::copy(sum.begin(), sum.end(), reinterpret_cast<DeviceSummary*>(out));
+    });
+}
+
 pascal_status pascal_sweep(const pascal_trace* t, const pascal_profile* p,
                            const pascal_run_config* base, const char* const* policies,
                            size_t n_policies, const double* fractions, size_t n_fractions,
                            const char* out_dir) {
+    return pascal_sweep_devices(t, p, base, policies, n_policies, fractions, n_fractions, out_dir,
+                                nullptr, 0);
+}
+
+pascal_status pascal_sweep_devices(const pascal_trace* t, const pascal_profile* p,
+                                   const pascal_run_config* base, const char* const* policies,
+                                   size_t n_policies, const double* fractions, size_t n_fractions,
+                                   const char* out_dir, const int* devices, int n_devices) {
     return guarded([&] {
         need(t && p && base && policies && fractions && out_dir, "null argument");
         need(n_policies >= 1 && n_fractions >= 1, "sweep needs at least one point");
@@ -435,12 +577,9 @@ pascal_status pascal_sweep(const pascal_trace* t, const pascal_profile* p,
         }
         for (const pascal_run_config& c : cfgs) jobs.push_back(Job{&t->t, to_cfg(&c), p->p});
         if (!device_available()) throw std::logic_error("no CUDA device available for the B200 engine");
-        std::unique_ptr<Batch, void (*)(Batch*)> b(batch_create(jobs), batch_free);
-        batch_execute(b.get());
         std::vector<DeviceSummary> sum;
-        batch_summaries(b.get(), sum);
         std::vector<std::vector<Row>> rows;
-        batch_rows(b.get(), rows);
+        run_jobs_devices(jobs, device_list(devices, n_devices), sum, &rows);
         std::error_code ignored;
         std::filesystem::create_directories(out_dir, ignored);
         std::string index =

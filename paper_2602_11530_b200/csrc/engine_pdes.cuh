@@ -103,15 +103,6 @@ DEVI void pdes_merge_peak(PdesCtl* ctl, const char* prec_all, int stride, int W)
     if (best != LLONG_MIN) atomicMax(&ctl->peak, best);
 }
 
-// End of phase A: all W warps meet on named barrier 1 (barrier 0 is
-// __syncthreads). Warp 0 arrives from inside its event loop, the others after
-// leaving theirs; bar.sync orders every warp's shared-memory writes before
-// warp 0's phase-B reads.
-DEVI void pdes_phase_barrier(int W) {
-    __syncwarp();
-    asm volatile("bar.sync 1, %0;" ::"r"(W * 32) : "memory");
-}
-
 template <bool TAIL_FAST>
 DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs, int c_smem,
                            int W) {
@@ -327,31 +318,28 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
         }
 
         // ---- one event loop (a single inlined copy of the handlers and the
-        // planner): phase A events, then phase B events on warp 0
+        // planner) run in two passes: pass 0 = phase A (every warp, its own
+        // instances' events before H), pass 1 = phase B (warp 0: the event at
+        // H). The CTA barrier between the passes (one PC for every warp)
+        // orders every warp's phase-A shared-memory writes before warp 0's
+        // phase-B reads, and phase B's writes before the next round.
         S.prec_n = 0;
-        S.phase_b = false;
         int ii = warp;
         bool b_started = false, b_over = false;
-        while (true) {
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          S.phase_b = pass == 1;
+          while (true) {
             HeapEnt e;
             int inst = -1;
             if (!S.phase_b) {
                 while (ii < ni && !(S.status == 0 && R.s.hn[ii] > 0 && inst_heap(R, ii)[1].t < H))
                     ii += W;
-                if (ii < ni) {
-                    inst = ii;
-                    e = heap_pop_inst(R, ii);
-                } else {
-                    if (warp != 0) break;
-                    // warp 0: wait until every other warp is quiescent (named
-                    // barrier 1; the other warps arrive after their phase A)
-                    if (W > 1) pdes_phase_barrier(W);
-                    if (bact == 0 || S.status != 0) break;
-                    S.phase_b = true;
-                }
-            }
-            if (S.phase_b) {
-                if (b_over) break;
+                if (ii >= ni) break;
+                inst = ii;
+                e = heap_pop_inst(R, ii);
+            } else {
+                if (warp != 0 || bact == 0 || S.status != 0 || b_over) break;
                 if (bact == 1) {
                     b_over = true;
                     e.t = TA;
@@ -416,8 +404,9 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
             maybe_start<TAIL_FAST>(R, S, plan_inst);
             if (oracle) peak_record(R, S, false);
             if (S.status != 0 && !S.phase_b && warp != 0) break;
+          }
+          __syncthreads();
         }
-        if (warp != 0) pdes_phase_barrier(W);  // releases warp 0 into phase B
         if (lane_id() == 0) {
             ctl->wrec[warp] = S.prec_n;
             if (S.status != 0) atomicCAS(&ctl->status, 0, S.status);

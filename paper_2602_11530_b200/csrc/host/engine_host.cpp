@@ -993,6 +993,19 @@ RunOutputs run_single(const Job& job, bool want_records, bool want_log) {
                                                              64 * (long long)job.trace->size())
                              : 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
+        if (want_log) {
+            // the decision log is kept on the device for the whole run (one
+            // 24-byte entry per line): refuse up front with a clear message
+            // instead of failing inside the allocator
+            size_t free_b = 0, total_b = 0;
+            if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
+                (double)cap * sizeof(pb::LogEnt) > 0.8 * (double)free_b)
+                throw std::runtime_error(
+                    "decision log of " + std::to_string(cap) + " entries (" +
+                    std::to_string((double)cap * sizeof(pb::LogEnt) / 1e9) +
+                    " GB) does not fit in device memory; run without an event log or split "
+                    "the trace");
+        }
         Batch b({job});
         if (want_records) b.enable_records();
         if (want_log) b.enable_log(cap);

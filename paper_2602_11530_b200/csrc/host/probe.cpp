@@ -106,6 +106,13 @@ void probe_maybe_start(const pascal_probe_state& st, const pb::Profile& prof,
     };
     scan(st.high_queue, st.n_high, 1);
     scan(st.low_queue, st.n_low, 2);
+    // baselines enqueue only at arrival (engine.cpp:111-116,260-283), so their
+    // queue is in arrival order; the engine's FCFS / oracle order is the queue
+    // order
+    if (policy != pb::kPascal)
+        for (long k = 1; k < st.n_high; ++k)
+            need(st.high_queue[k - 1] < st.high_queue[k],
+                 "baseline queue not in arrival order (baselines enqueue only at arrival)");
     std::sort(queued.begin(), queued.end());
     std::vector<unsigned> dseq(n, 0);  // engine seqs: unique, same relative order
     for (size_t k = 0; k < queued.size(); ++k) dseq[queued[k].second] = (unsigned)(k + 1);

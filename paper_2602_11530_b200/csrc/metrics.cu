@@ -250,12 +250,10 @@ int launch_histograms(const int* rid, const int* group, const RowArrays rows,
     if (total > 0) {
         const size_t smem = sizeof(unsigned) * (size_t)n_groups * (kHistBins + 4);
         if (smem <= 96 * 1024) {
-            static bool attr = false;  // opt in above 48 KB once per process
-            if (!attr) {
-                cudaFuncSetAttribute(hist_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     96 * 1024);
-                attr = true;
-            }
+            // opt in above 48 KB (a per-device function attribute: set on
+            // every launch, the batch may live on any device)
+            cudaFuncSetAttribute(hist_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 96 * 1024);
             int dev = 0, sms = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -13,7 +13,8 @@ from harness import (build_trace, first_diff, golden, make_cfg, make_profile, or
                      sha_file)
 
 GOLD = golden()
-PARAMS = [c for c in CASES if c["name"] in GOLD and c["size"] not in ("large", "xlarge")]
+PARAMS = [c for c in CASES if c["name"] in GOLD
+          and c["size"] not in ("large", "xlarge", "huge", "thrash")]
 
 
 @pytest.mark.gpu
@@ -63,16 +64,19 @@ def test_large_bit_exact(c, tmp_path):
         assert sha_file(f"{prefix}.{ext}") == want, ext
 
 
-XLARGE = [c for c in CASES if c["name"] in GOLD and c["size"] == "xlarge"]
+XLARGE = [c for c in CASES if c["name"] in GOLD and c["size"] in ("xlarge", "thrash")
+          and "records" in GOLD[c["name"]]]
 
 
 @pytest.mark.gpu
 @pytest.mark.slow
 @pytest.mark.parametrize("c", XLARGE, ids=[c["name"] for c in XLARGE])
 def test_xlarge_records_and_reports(c, tmp_path):
-    """C3 (BASELINE.json configs[2]: 20k requests, 8 instances) and a
-    C4-shaped 64-instance run: every RequestRecord double and every report
-    byte equal to the reference's (decision logs not materialised)."""
+    """C3 (BASELINE.json configs[2]: 20k requests, 8 instances, the arrival-
+    rate sweep and the capacity-0.5 stress point), a C4-shaped 64-instance
+    run and the C5 thrash rates k < 3 (configs[4]): every RequestRecord double
+    and every report byte equal to the reference's (decision logs not
+    materialised)."""
     g = GOLD[c["name"]]
     t = build_trace(c["trace"])
     rec = str(tmp_path / "gpu.rec")
@@ -108,3 +112,58 @@ def test_instance_parallel_records_bit_exact(c, tmp_path):
                     first_diff(rec, orec))
     if len(t) > 0:
         assert used in (0, 1)
+
+
+HUGE = [c for c in CASES if c["name"] in GOLD and c["size"] == "huge"
+        and "records" in GOLD[c["name"]]]
+
+
+def sha_stream(writer):
+    """sha256 + line count of what `writer(path)` writes to `path`, through a
+    FIFO (C4's records are ~26 GB of text and are never stored)."""
+    import hashlib
+    import tempfile
+    import threading
+    d = tempfile.mkdtemp()
+    fifo = os.path.join(d, "rec.fifo")
+    os.mkfifo(fifo)
+    res = {}
+
+    def reader():
+        h = hashlib.sha256()
+        n = 0
+        with open(fifo, "rb") as f:
+            while True:
+                b = f.read(1 << 22)
+                if not b:
+                    break
+                h.update(b)
+                n += b.count(b"\n")
+        res["sha"] = [h.hexdigest(), n]
+
+    th = threading.Thread(target=reader)
+    th.start()
+    try:
+        writer(fifo)
+    finally:
+        th.join()
+        os.unlink(fifo)
+        os.rmdir(d)
+    return res["sha"]
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.skipif(not os.environ.get("PB_SLOW"), reason="C4 at 1M requests: set PB_SLOW=1")
+@pytest.mark.parametrize("c", HUGE, ids=[c["name"] for c in HUGE])
+def test_c4_full_records_and_reports(c, tmp_path):
+    """C4 at its stated size (BASELINE.json configs[3]: mixed preset, 1M
+    requests, 64 instances, lambda 16, capacity 0.9)."""
+    g = GOLD[c["name"]]
+    t = build_trace(c["trace"])
+    got = sha_stream(lambda path: pb.run_dump(t, make_profile(c), make_cfg(c), path, None))
+    assert got == g["records"]
+    prefix = str(tmp_path / "rep")
+    pb.run(t, make_profile(c), make_cfg(c), prefix)
+    for ext, want in g["report"].items():
+        assert sha_file(f"{prefix}.{ext}") == want, ext

@@ -181,7 +181,11 @@ def random_state(rng: random.Random, policy: str):
         reqs.append(r)
     high, low = [], []
     seq = 0
-    for k in rng.sample(range(n), n):  # enqueue order
+    # enqueue order: baselines enqueue only at arrival (their queue is in
+    # arrival order, engine.cpp:111-116,260-283); Pascal's low queue fills in
+    # event order (transitions, demotions, transfers)
+    order = rng.sample(range(n), n) if policy == "pascal" else list(range(n))
+    for k in order:
         if rng.random() < 0.1:
             continue  # not queued
         r = reqs[k]
