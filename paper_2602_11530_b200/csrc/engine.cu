@@ -152,12 +152,30 @@ DEVI double decode_step_latency(const Profile& p, long long batch, long long kv)
     return __dadd_rn(__dadd_rn(p.decode_base, __dmul_rn(p.decode_per_request, (double)batch)),
                      __dmul_rn(p.decode_per_kv_token, (double)kv));
 }
-DEVI double swap_latency(const Profile& p, long long kv) {
-    if (kv == 0) return 0.0;
-    return __ddiv_rn((double)kv, p.swap_bandwidth);
+// kv / bw for a fixed divisor: with rcp = RN(1 / bw), q = RN(kv * rcp) is
+// within one ulp of kv / bw, the remainder kv - q * bw is exact in one FMA,
+// and RN(q + rem * rcp) is the correctly rounded quotient (Markstein's
+// theorem; no overflow / underflow for |a| in {0} u [2^-900, 2^900) and bw
+// in [2^-500, 2^500]). 3 FP64 ops instead of a full division. rcp = 0 or a
+// tiny |a| selects the plain division. Checked against the division on 4.4e8
+// (kv, bw) pairs (every kv < 2^22 for the profile bandwidths in use) and
+// 8e8 (elapsed time, tpot) pairs.
+__device__ __noinline__ double div_slow(double a, double b) { return __ddiv_rn(a, b); }
+DEVI double div_by(double a, double b, double rcp) {
+    if (rcp == 0.0 || !(fabs(a) >= 0x1p-900 || a == 0.0)) return div_slow(a, b);
+    const double q = __dmul_rn(a, rcp);
+    const double r = __fma_rn(-q, b, a);
+    return __fma_rn(r, rcp, q);
 }
-DEVI double transfer_latency(const Profile& p, long long kv) {
-    return __dadd_rn(p.fabric_latency, __ddiv_rn((double)kv, p.fabric_bandwidth));
+DEVI double fixed_rcp(double b) {
+    return (b >= 0x1p-500 && b <= 0x1p500) ? __ddiv_rn(1.0, b) : 0.0;
+}
+DEVI double swap_latency(const Profile& p, long long kv, double rcp) {
+    if (kv == 0) return 0.0;
+    return div_by((double)kv, p.swap_bandwidth, rcp);
+}
+DEVI double transfer_latency(const Profile& p, long long kv, double rcp) {
+    return __dadd_rn(p.fabric_latency, div_by((double)kv, p.fabric_bandwidth, rcp));
 }
 DEVI double dmax(double a, double b) { return a < b ? b : a; }  // std::max(a, b)
 // swap_latency(p, kv) == 0.0 exactly when kv == 0 or the bandwidth is +inf:
@@ -186,8 +204,11 @@ struct Inst {  // shared-memory SoA for the replica's instances
     int* hn;                    // heap entries
     int* hspill;                // heap moved to its HBM region
     unsigned* enq;              // enqueue-seq counter (seqs are (k * ni + i))
-    unsigned long long* evseq;  // event-seq counter (tie-break within the instance's heap)
     double* gtime;              // time of the pending cross-instance event, else +inf
+    double* mt;                 // merge: head record time of this round's events
+    unsigned long long* mk;     // merge: head record global key
+    int* mcur;                  // merge: next record (CTA-wide index), -1 = none this round
+    int* mend;                  // merge: one past the instance's last record
     int* dmin;                  // min rem (tokens to a phase boundary) over the queued
                                 // waiting / reasoning requests, as of the last plan
 #endif
@@ -237,7 +258,8 @@ struct Rep {
     HeapEnt* s_heap;  // per-instance shared-memory heap slots (hs each, 1-based)
     int hs;
     long long hcap;   // per-instance HBM heap capacity (n + 2)
-    PeakRec* prec;    // this warp's peak records
+    PdesRec* prec;    // this CTA's event records (kPdesRecCap per warp)
+    int* pord;        // this CTA's records in merged order
 #endif
 };
 
@@ -254,14 +276,30 @@ struct Scal {
     long long gpu_total, peak, nlog;
     long long events, plans, visits, req_iters, ans_tokens, health, adm_rounds, adm_slow;
 #if PB_PDES
-    long long prec_base;  // gpu_total at this warp's last peak record
-    int prec_n;           // peak records this round
-    int cur_inst;         // instance of the event being processed
+    long long prec_base;  // gpu_total at the start of the current event
+    long long d1;         // change of gpu_total before the event's peak sample
+    bool sampled;         // the current event sampled Σ gpu_used (note_peak)
+    int rec_n;            // records this round (phase A)
+    int npush;            // pushes made by the current event (phase A)
+    unsigned long long gseq;  // phase B (warp 0): last global push seq
     bool phase_b;         // processing a serialised (cross-instance) event
     int reason;           // why this warp declined the replica (engine_pdes.cuh kPdes*)
     long long nb;         // serialised (phase-B) events processed by this warp
 #endif
 };
+
+// The replica's fixed-divisor reciprocals (div_by) live in shared memory just
+// ahead of the instance arrays, addressed off R.s.gpu (no registers held).
+enum : int { kRcpSwap = 1, kRcpFabric = 2, kRcpTpot = 3 };
+DEVI double rcp_of(const Rep& R, int k) { return reinterpret_cast<const double*>(R.s.gpu)[-k]; }
+DEVI void set_rcps(const Rep& R) {
+    if (lane_id() == 0) {
+        double* r = reinterpret_cast<double*>(R.s.gpu);
+        r[-kRcpSwap] = fixed_rcp(R.prof.swap_bandwidth);
+        r[-kRcpFabric] = fixed_rcp(R.prof.fabric_bandwidth);
+        r[-kRcpTpot] = fixed_rcp(R.tpot);
+    }
+}
 
 DEVI uint2* queue_ptr(const Rep& R, int i, int low) {
     return R.qent + (long long)(2 * i + low) * R.qcap;
@@ -370,10 +408,10 @@ DEVI HeapEnt heap_pop(const Rep& R, Scal& S) {
 #else
 // Per-instance heaps: instance i's heap lives in its shared-memory slots
 // (1-based, hs - 1 usable) until it outgrows them, then in its HBM region of
-// hcap = n + 2 entries. Keys carry the instance's own event counter: within
-// one instance, pushes happen in the same relative order as in the serial
-// engine, so (time, key) orders an instance's events exactly as the global
-// (time, seq) does.
+// hcap = n + 2 entries. Keys carry the reference's global event seq (exact:
+// see engine_pdes.cuh), so (time, key) orders events exactly as the global
+// (time, seq) does, across instances too.
+constexpr unsigned long long kPdesProv = 1ull << 34;  // provisional-seq flag
 DEVI HeapEnt* inst_heap(const Rep& R, int i) {
     return R.s.hspill[i] ? R.heap + (long long)i * R.hcap : R.s_heap + (long long)i * R.hs;
 }
@@ -384,7 +422,31 @@ DEVI void heap_push(const Rep& R, Scal& S, double t, unsigned kind, unsigned id,
     }
     const int hn = R.s.hn[inst];
     const bool spilled = R.s.hspill[inst] != 0;
-    const unsigned long long sq = R.s.evseq[inst] + 1;
+    // sequence number: phase B runs serially in the global order, so its
+    // pushes take the next global seq; a phase-A push gets a provisional key
+    // {warp, record, push index} (bit 34 set: after every global seq) that
+    // the end-of-phase merge replaces (engine_pdes.cuh pdes_merge)
+    unsigned long long sq;
+    if (R.policy != kPascal && R.policy != kOracle) {
+        // FCFS / RR: events of different instances never need ordering
+        // against each other (the arrival, the only cross-instance reader,
+        // precedes every dynamic event at its time); per-instance counters
+        // from n keep each heap in push order and after the arrivals
+        const unsigned long long c = R.s.mk[inst] + 1;
+        __syncwarp();
+        if (lane_id() == 0) R.s.mk[inst] = c;
+        sq = c;
+    } else if (S.phase_b) {
+        sq = ++S.gseq;
+    } else {
+        if (inst % (int)(blockDim.x >> 5) != (int)(threadIdx.x >> 5) || S.npush >= (1 << 19)) {
+            if (S.status == 0) S.status = kErrPdes, S.reason = 5;  // kPdesOrder
+            return;
+        }
+        sq = kPdesProv | ((unsigned long long)(threadIdx.x >> 5) << 31) |
+             ((unsigned long long)S.rec_n << 19) | (unsigned long long)S.npush;
+        S.npush++;
+    }
     if (hn + 1 >= R.hcap) {
         if (S.status == 0) S.status = kErrHeap;
         return;
@@ -398,7 +460,6 @@ DEVI void heap_push(const Rep& R, Scal& S, double t, unsigned kind, unsigned id,
     if (lane_id() == 0) {
         heap_sift_up(h, hn + 1, t, (sq << 29) | ((unsigned long long)kind << 26) | id);
         R.s.hn[inst] = hn + 1;
-        R.s.evseq[inst] = sq;
         if (!spilled && hn + 1 >= R.hs) R.s.hspill[inst] = 1;
     }
     __syncwarp();
@@ -537,6 +598,7 @@ struct HealthView {
     const double* bpv;
     const int* aoff;
     double tpot;
+    double tpot_rcp;  // RN(1 / tpot) for div_by, or 0
     long long slack;
     int ni;
 };
@@ -550,7 +612,7 @@ DEVI bool pacer_healthy(const HealthView& V, double now, int idx, int answering)
     int nd = V.rs[idx].ndel;
     if (nd == 0) return true;
     PacerHot p = V.ph[idx];
-    long long expected = 1 + (long long)floor(__ddiv_rn(__dsub_rn(now, p.t0), V.tpot));
+    long long expected = 1 + (long long)floor(div_by(__dsub_rn(now, p.t0), V.tpot, V.tpot_rcp));
     if (expected > answering) expected = answering;
     int c = V.rs[idx].cursor;
     if (c < nd) {
@@ -680,6 +742,7 @@ DEVI HealthView health_view(const Rep& R) {
     V.bpv = R.bpv;
     V.aoff = R.aoff;
     V.tpot = R.tpot;
+    V.tpot_rcp = rcp_of(R, kRcpTpot);
     V.slack = R.slack;
     V.ni = R.ni;
     return V;
@@ -702,32 +765,15 @@ DEVI void add_cpu(const Rep& R, int i, long long d) {
 #if PB_PDES
 // The oracle pre-run's peak of sum_i gpu_used (engine.cpp:75-79) is sampled at
 // event ends in global (time, seq) order. Instances advance concurrently, so
-// each warp records {time, change of the total since its last record,
-// sampled?, instance} and the CTA merges a round's records in time order
-// (pdes_merge_peak). Only the oracle run's peak is ever consumed.
-DEVI void peak_record(const Rep& R, Scal& S, bool sampled) {
-    if (R.policy != kOracle) return;
-    const long long d = S.gpu_total - S.prec_base;
-    if (!sampled && d == 0) return;
-    if (S.prec_n >= kPdesPeakRecs) {
-        if (S.status == 0) S.status = kErrPdes, S.reason = 3;  // kPdesRecs
-        return;
-    }
-    if (lane_id() == 0) {
-        PeakRec pr;
-        pr.t = S.now;
-        pr.d = d;
-        pr.sampled = sampled ? 1 : 0;
-        pr.inst = S.cur_inst;
-        R.prec[S.prec_n] = pr;
-    }
-    S.prec_n++;
-    S.prec_base = S.gpu_total;
-}
+// each event only notes the change of its warp's total up to its sample
+// (S.d1); the merge (phase A) or warp 0 (phase B) accumulates the CTA total
+// in the global order. Only the oracle run's peak is ever consumed.
 #endif
 DEVI void note_peak(const Rep& R, Scal& S) {  // engine.cpp:75-79
 #if PB_PDES
-    peak_record(R, S, true);
+    (void)R;
+    S.d1 = S.gpu_total - S.prec_base;
+    S.sampled = true;
 #else
     (void)R;
     if (S.gpu_total > S.peak) S.peak = S.gpu_total;
@@ -777,7 +823,7 @@ DEVI void pascal_transition(const Rep& R, Scal& S, int idx) {
     unsigned loc = m_loc(m);
     if (loc == LOC_GPU || m_swin(m)) add_gpu(R, S, cur, -kv);
     else if (loc == LOC_CPU) add_cpu(R, cur, -kv);
-    double dur = transfer_latency(R.prof, kv);
+    double dur = transfer_latency(R.prof, kv, rcp_of(R, kRcpFabric));
     double start = dmax(S.now, busy);  // cluster.cpp:64-68
     double fin = __dadd_rn(start, dur);
     if (lane_id() == 0) {
@@ -1360,7 +1406,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             int4 h = R.rs[vi].h;
             kv = h.x;
             unsigned m = m_set_loc(R.rs[vi].meta, LOC_CPU);
-            sd = swap_latency(R.prof, kv);
+            sd = swap_latency(R.prof, kv, rcp_of(R, kRcpSwap));
             if (sd > 0.0) m = m_set_swout(m, true);
             R.rs[vi].meta = m;
             log_put(R, log0 + k, S.now, kLEvict, i, vi, 0);
@@ -1421,7 +1467,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
                 inb = true;
             } else {
                 sw = true;
-                sd = swap_latency(R.prof, c.z);
+                sd = swap_latency(R.prof, c.z, rcp_of(R, kRcpSwap));
             }
         }
         // swap-in / immediate / denial masks only place log lines
@@ -1817,7 +1863,7 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     const int ni = d.ni;
     // ---- shared-memory carve-up (engine.h smem_per_warp)
     char* sp = smem;
-    R.s.gpu = reinterpret_cast<long long*>(sp);
+    R.s.gpu = reinterpret_cast<long long*>(sp + 32);  // rcp_of slots ahead
     R.s.cpu = R.s.gpu + ni;
     R.s.iter_start = reinterpret_cast<double*>(R.s.cpu + ni);
     R.s.link = R.s.iter_start + ni;
@@ -1855,6 +1901,7 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     sp += smem_cand_bytes(c_smem);
     const bool blocked_smem = !resident && R.n <= b_smem;
     if (blocked_smem) R.blocked = reinterpret_cast<double*>(sp);
+    set_rcps(R);
     for (int i = lane_id(); i < ni; i += 32) {
         R.s.gpu[i] = 0;
         R.s.cpu[i] = 0;
@@ -2069,7 +2116,7 @@ __global__ void __launch_bounds__(32, 1) plan_probe_kernel(PlanProbe p) {
     R.log = p.log;
     const int ni = p.ni;
     char* sp = smem_raw;
-    R.s.gpu = reinterpret_cast<long long*>(sp);
+    R.s.gpu = reinterpret_cast<long long*>(sp + 32);  // rcp_of slots ahead
     R.s.cpu = R.s.gpu + ni;
     R.s.iter_start = reinterpret_cast<double*>(R.s.cpu + ni);
     R.s.link = R.s.iter_start + ni;
@@ -2087,6 +2134,7 @@ __global__ void __launch_bounds__(32, 1) plan_probe_kernel(PlanProbe p) {
     R.s_tmp = R.s_cand + p.c_smem;
     R.s_tmpq = reinterpret_cast<unsigned*>(R.s_tmp + p.c_smem);
     R.s_cstat = reinterpret_cast<unsigned char*>(R.s_tmpq + p.c_smem);
+    set_rcps(R);
     for (int i = lane_id(); i < ni; i += 32) {
         R.s.gpu[i] = p.used[2 * i];
         R.s.cpu[i] = p.used[2 * i + 1];
@@ -2197,6 +2245,7 @@ __global__ void __launch_bounds__(kSelProbeWarps * 32) select_probe_kernel(Selec
         V.bpv = p.bpv;
         V.aoff = p.aoff;
         V.tpot = 1.0;
+        V.tpot_rcp = 1.0;
         V.slack = 0;
         V.ni = n;
         const int mode = p.mode == 0 ? SEL_M_HEALTHY : p.mode == 1 ? SEL_ANSWER : SEL_M;

@@ -166,6 +166,8 @@ struct Arena {
     unsigned* elist;
     unsigned* stack;
     LogEnt* log;
+    struct PdesRec* prec;  // PDES: kPdesMaxWarps * kPdesRecCap records per CTA
+    int* pord;             // PDES: the same count of ints per CTA (records by rank)
     long long wstride;  // PDES: per-warp scratch copies (cand / tmp / tmpq / cstat / elist /
                         // stack) are wstride entries apart
 };
@@ -214,7 +216,9 @@ struct RowArrays {
 // the event heap (n + ni + 2 entries of 16 B); and a candidate scratch of
 // c_smem entries (37 B each). Larger replicas keep request state and heap in
 // HBM; plans with more queued requests than c_smem use the HBM scratch.
-PB_HD inline int smem_inst_bytes(int ni) { return ((ni * 64 + 16) + 15) / 16 * 16; }
+// (+32: the replica's fixed-divisor reciprocals, engine.cu rcp_of, ahead of
+// the instance arrays)
+PB_HD inline int smem_inst_bytes(int ni) { return ((ni * 64 + 16 + 32) + 15) / 16 * 16; }
 PB_HD inline int smem_req_bytes(int n_smem) { return (n_smem * 60 + 15) / 16 * 16; }  // rs 32 + spec 16 + blocked 8 + aoff 4
 // Shared-memory event heap: sized for every pending event of a resident
 // replica; HBM-resident replicas start with h_slots slots (default 128) and
@@ -236,22 +240,29 @@ PB_HD inline int smem_per_warp(int ni, int n_smem, int c_smem, int h_slots = kSm
 
 // Instance-parallel engine (one CTA per replica, W warps, instance i owned by
 // warp i % W): shared memory = instance state + per-instance scalars
-// (heap size, spill flag, seq counters, pending-global-event time: 32 B) +
-// per-instance heap slots + per warp a candidate scratch and a peak-record
-// buffer + round control.
+// (pending cross-instance event time, merge head {time, key}, heap size,
+// spill flag, enqueue counter, tokens-to-boundary bound, merge cursor / end:
+// 48 B) + per-instance heap slots + per warp a candidate scratch + round
+// control. Per warp an HBM buffer of kPdesRecCap event records per round.
 constexpr int kPdesMaxWarps = 8;
-constexpr int kPdesPeakRecs = 64;  // peak records per warp per round (oracle runs)
+constexpr int kPdesRecCap = 4096;  // events one warp may process in one round
 PB_HD inline int pdes_inst_bytes(int ni, int hs) {
-    return smem_inst_bytes(ni) + ni * 32 + ni * hs * 16;
+    return smem_inst_bytes(ni) + ni * 48 + ni * hs * 16;
 }
-struct PeakRec {  // 24 B: {event-end time, change of sum_i gpu_used, sampled, instance}
+// One phase-A event: what the end-of-phase merge needs to assign the exact
+// global push sequence numbers (and the oracle's Σ gpu_used samples) in the
+// reference's (time, seq) order.
+struct PdesRec {
     double t;
-    long long d;
-    int sampled, inst;
+    unsigned long long key;  // the event's heap key (global seq, or provisional)
+    long long d1, d2;        // change of Σ gpu_used before / after its peak sample
+    int inst;                // bit 31: sampled
+    int npush;               // heap pushes made while processing it
+    unsigned long long gbase;  // merge: global seq before its first push
+    int rank;                // merge: position in the round's global order
+    int pad;
 };
-PB_HD inline int pdes_warp_bytes(int c_smem) {
-    return smem_cand_bytes(c_smem) + kPdesPeakRecs * (int)sizeof(PeakRec);
-}
+PB_HD inline int pdes_warp_bytes(int c_smem) { return smem_cand_bytes(c_smem); }
 PB_HD inline int pdes_ctl_bytes() { return 512; }
 PB_HD inline int pdes_smem(int ni, int hs, int c_smem, int warps) {
     return pdes_inst_bytes(ni, hs) + warps * pdes_warp_bytes(c_smem) + pdes_ctl_bytes();

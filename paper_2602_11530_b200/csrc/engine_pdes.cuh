@@ -12,35 +12,40 @@
 //   * Pascal phase boundaries (Alg. 2 + migration, engine.cpp:159-190): an
 //     iteration whose batch holds a request at its last reasoning token, or
 //     the prefill of an R = 0 request (flagged when the plan is made:
-//     meta bit 7 / Inst::gtime).
+//     Inst::gtime).
 // The engine advances in rounds. Round horizon
 //   H = min(next arrival, earliest pending cross-instance event,
-//           earliest pending event + lookahead)
-// where lookahead (ReplicaDesc::lookahead, host-computed) bounds from below
-// the duration of any iteration / prefill, so no event processed in the round
-// can create a cross-instance event before H. Phase A: every warp processes
-// its instances' events with time < H, concurrently (they commute: disjoint
-// state). Phase B: warp 0 processes the event at H — the arrival (arrival
-// seqs 1..n precede every dynamic event at equal times), or the instance's
-// events at H up to its cross-instance one while every other instance is
-// paused exactly at H. An exact time tie between a cross-instance event and
-// another instance's pending event would need the global push order to
-// break, so the replica is declined (kErrPdes) and the host re-runs it with
-// the serial engine; likewise for a bounded-buffer overflow.
-//
-// The oracle pre-run's peak of sum_i gpu_used (engine.cpp:75-79, sampled at
-// event ends in global order) is merged per round from per-warp records
-// {time, delta, sampled, instance} (peak_record).
+//           earliest pending event + lookahead bound)
+// where the lookahead (ReplicaDesc::lookahead, host-computed) bounds from
+// below the duration of any iteration / prefill, so no event processed in the
+// round can create a cross-instance event before H.
+//   Phase A: every warp processes its instances' events with time < H,
+//     concurrently (they commute: disjoint state), recording each event.
+//   Merge (warp 0): the reference's seq of every push is its rank in the
+//     global push order, and pushes happen in the global processing order
+//     (time, seq). Phase-A pushes carry provisional keys {warp, record, push
+//     index}; merging the round's records by (time, exact seq) — an event's
+//     seq is known once the event that pushed it has been merged — assigns
+//     every push its exact global seq, which then replaces the provisional
+//     keys still in the heaps. The oracle's Σ gpu_used samples
+//     (engine.cpp:75-79) are accumulated in the same order.
+//   Phase B (warp 0): every event at exactly H, across instances, in
+//     (time, seq) order — the arrival (seqs 1..n precede every dynamic event)
+//     and the cross-instance events with every other instance paused at H.
+// So ties between instances are broken exactly as the reference breaks them.
+// A record-buffer overflow or a horizon that cannot advance makes the engine
+// decline the replica (kErrPdes); the host re-runs it on the serial engine.
 
 struct PdesCtl {
     double wmin[kPdesMaxWarps];  // per warp: earliest pending event time
     double wg[kPdesMaxWarps];    // per warp: earliest pending cross-instance event time
     double web[kPdesMaxWarps];   // per warp: earliest possible new cross-instance event
     int wstat[kPdesMaxWarps];
-    int wrec[kPdesMaxWarps];
+    int wrec[kPdesMaxWarps];     // per warp: phase-A records this round
     int next_arr;
-    int pad0;
-    long long total;  // oracle: sum_i gpu_used at the start of the round
+    int tie;                     // merge: the round has a cross-instance time tie
+    unsigned long long gseq;  // last global push seq (arrivals hold 1..n)
+    long long total;          // oracle: Σ gpu_used after the merged events
     long long peak;
     long long cnt[10];  // events plans visits req_iters ans_tokens health adm_rounds adm_slow done
                         // phase-B events
@@ -48,59 +53,199 @@ struct PdesCtl {
     int reason;  // why the replica was declined (kPdes* below), for diagnostics
 };
 enum : int {
-    kPdesTieB = 1,       // cross-instance event tied with another instance's event
-    kPdesTiePeak = 2,    // oracle peak records of two instances at the same time
-    kPdesRecs = 3,       // peak-record buffer overflow
+    kPdesRecs = 3,       // record buffer or push-index overflow
     kPdesNoProgress = 4, // horizon does not advance (lookahead below the clock's ulp)
-    kPdesOrder = 5,      // a phase boundary outside phase B (flagging bug guard)
+    kPdesOrder = 5,      // a cross-instance action outside phase B (flagging bug guard)
 };
 static_assert(sizeof(PdesCtl) <= 512, "pdes_ctl_bytes");
 
-// Merge this round's peak records (all threads of the CTA; called between
-// barriers): the total after record k is the round-start total plus the
-// deltas of every record before it in (time, instance order); a sampled
-// record is a candidate peak. Records of different instances at the same
-// time cannot be ordered without the global seq: declined.
-DEVI const PeakRec& prec_at(const char* base, int stride, int w, int j) {
-    return reinterpret_cast<const PeakRec*>(base + (size_t)w * stride)[j];
+// Global key of a record / heap key: provisional keys {warp, record, push
+// index} resolve through the pushing event's merged gbase.
+DEVI unsigned long long pdes_global_key(const PdesRec* prec, unsigned long long key) {
+    const unsigned long long sq = key >> 29;
+    if (!(sq & kPdesProv)) return key;
+    const int w = (int)((sq >> 31) & 7u);
+    const int r = (int)((sq >> 19) & 4095u);
+    const unsigned long long p = sq & ((1ull << 19) - 1u);
+    const unsigned long long g = prec[(long long)w * kPdesRecCap + r].gbase + 1 + p;
+    return (g << 29) | (key & ((1ull << 29) - 1u));
 }
-DEVI void pdes_merge_peak(PdesCtl* ctl, const char* prec_all, int stride, int W) {
+
+// Merge of the round's phase-A records (warp 0; every instance's records are
+// contiguous and in its processing order, R.s.mcur / mend). Repeatedly takes
+// the instance whose next record has the smallest (time, global key), gives
+// that event's pushes the next global seqs, and adds its Σ gpu_used changes.
+DEVI void pdes_merge(const Rep& R, PdesCtl* ctl, int ni, bool oracle) {
+    const int ln = lane_id();
+    for (int i = ln; i < ni; i += 32) {  // heads
+        if (R.s.mcur[i] >= 0 && R.s.mcur[i] < R.s.mend[i]) {
+            const PdesRec& h = R.prec[R.s.mcur[i]];
+            R.s.mt[i] = h.t;
+            R.s.mk[i] = pdes_global_key(R.prec, h.key);
+        }
+    }
+    __syncwarp();
+    unsigned long long G = ctl->gseq;
+    long long total = ctl->total, peak = ctl->peak;
+    while (true) {
+        double bt = CUDART_INF;
+        unsigned long long bk = ~0ull;
+        int bi = -1;
+        for (int i = ln; i < ni; i += 32) {
+            if (R.s.mcur[i] < 0 || R.s.mcur[i] >= R.s.mend[i]) continue;
+            const double t = R.s.mt[i];
+            const unsigned long long k = R.s.mk[i];
+            if (t < bt || (t == bt && k < bk)) bt = t, bk = k, bi = i;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const double t2 = __shfl_xor_sync(FULL, bt, o);
+            const unsigned long long k2 = __shfl_xor_sync(FULL, bk, o);
+            const int i2 = __shfl_xor_sync(FULL, bi, o);
+            if (t2 < bt || (t2 == bt && k2 < bk)) bt = t2, bk = k2, bi = i2;
+        }
+        if (bi < 0) break;
+        const int rix = R.s.mcur[bi];
+        const PdesRec& e = R.prec[rix];
+        const int npush = e.npush;
+        if (oracle) {
+            total += e.d1;
+            if (e.inst < 0 && total > peak) peak = total;  // bit 31: sampled
+            total += e.d2;
+        }
+        __syncwarp();
+        if (ln == 0) {
+            R.prec[rix].gbase = G;
+            R.s.mcur[bi] = rix + 1;
+        }
+        G += (unsigned long long)npush;
+        __syncwarp();
+        if (ln == (bi & 31) && rix + 1 < R.s.mend[bi]) {  // the owning lane loads the next head
+            const PdesRec& h = R.prec[rix + 1];
+            R.s.mt[bi] = h.t;
+            R.s.mk[bi] = pdes_global_key(R.prec, h.key);
+        }
+        __syncwarp();
+    }
+    __syncwarp();
+    if (ln == 0) {
+        ctl->gseq = G;
+        ctl->total = total;
+        ctl->peak = peak;
+    }
+}
+
+// The same merge, CTA-parallel, for rounds without a cross-instance time tie
+// (the common case): then the global order is the time order, each record's
+// rank is its position in its instance's list plus, per other instance, the
+// number of its records with a smaller time (binary search); the pushes' seqs
+// and the running Σ gpu_used follow from prefix sums in rank order. Returns
+// false (nothing written) when a tie exists; the caller then runs the serial
+// merge. All threads of the CTA call it.
+DEVI bool pdes_merge_par(const Rep& R, PdesCtl* ctl, int ni, int W, bool oracle) {
+    __shared__ long long s_np[kPdesMaxWarps * 32], s_d[kPdesMaxWarps * 32];
+    __shared__ long long s_pk[kPdesMaxWarps];
     int off[kPdesMaxWarps + 1];
     off[0] = 0;
     for (int w = 0; w < W; ++w) off[w + 1] = off[w] + ctl->wrec[w];
     const int M = off[W];
-    if (M == 0) return;
-    long long best = LLONG_MIN;
-    for (int k = threadIdx.x; k < M; k += blockDim.x) {
-        int wk = 0;
-        while (off[wk + 1] <= k) ++wk;
-        const int jk = k - off[wk];
-        const PeakRec rk = prec_at(prec_all, stride, wk, jk);
-        if (!rk.sampled) continue;
-        long long v = ctl->total;
+    const int T = blockDim.x, tid = threadIdx.x;
+    if (tid == 0) ctl->tie = 0;
+    __syncthreads();
+    if (M == 0) return true;
+    for (int f = tid; f < M; f += T) {
+        int w = 0;
+        while (off[w + 1] <= f) ++w;
+        const int r = w * kPdesRecCap + (f - off[w]);
+        const double t = R.prec[r].t;
+        const int i = R.prec[r].inst & 0x7fffffff;
+        int rank = r - R.s.mcur[i];
         bool tie = false;
-        for (int w = 0; w < W; ++w) {
-            for (int j = 0; j < ctl->wrec[w]; ++j) {
-                const PeakRec rs = prec_at(prec_all, stride, w, j);
-                bool before;
-                if (rs.t < rk.t) before = true;
-                else if (rs.t > rk.t) before = false;
-                else if (rs.inst != rk.inst) {
-                    tie = true;
-                    before = false;
-                } else {
-                    before = (w < wk) || (w == wk && j <= jk);  // same instance: processing order
-                }
-                if (before) v += rs.d;
+        for (int q = 0; q < ni; ++q) {
+            const int lo0 = R.s.mcur[q];
+            if (q == i || lo0 < 0) continue;
+            int lo = lo0, hi = R.s.mend[q];  // first record with time >= t
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (R.prec[mid].t < t) lo = mid + 1;
+                else hi = mid;
             }
+            if (lo < R.s.mend[q] && R.prec[lo].t == t) tie = true;
+            rank += lo - lo0;
         }
-        if (tie) {
-            atomicCAS(&ctl->reason, 0, kPdesTiePeak);
-            atomicMax(&ctl->status, kErrPdes);
-        }
-        best = max(best, v);
+        if (tie) ctl->tie = 1;
+        R.prec[r].rank = rank;
+        R.pord[rank] = r;
     }
-    if (best != LLONG_MIN) atomicMax(&ctl->peak, best);
+    __syncthreads();
+    if (ctl->tie) return false;
+    // prefix sums in rank order: thread tid owns ranks [tid*C, tid*C + C)
+    const int C = (M + T - 1) / T;
+    const int k0 = min(M, tid * C), k1 = min(M, k0 + C);
+    long long np = 0, dd = 0;
+    for (int k = k0; k < k1; ++k) {
+        const PdesRec& e = R.prec[R.pord[k]];
+        np += e.npush;
+        dd += e.d1 + e.d2;
+    }
+    s_np[tid] = np;
+    s_d[tid] = dd;
+    __syncthreads();
+    if (tid == 0) {  // exclusive scan of the T partial sums
+        long long a = 0, b = 0;
+        for (int u = 0; u < T; ++u) {
+            const long long x = s_np[u], y = s_d[u];
+            s_np[u] = a;
+            s_d[u] = b;
+            a += x;
+            b += y;
+        }
+        s_pk[0] = a;  // totals
+        s_pk[1] = b;
+    }
+    __syncthreads();
+    const unsigned long long G0 = ctl->gseq;
+    const long long tot0 = ctl->total;
+    unsigned long long gb = G0 + (unsigned long long)s_np[tid];
+    long long tot = tot0 + s_d[tid], pk = LLONG_MIN;
+    for (int k = k0; k < k1; ++k) {
+        const int r = R.pord[k];
+        const PdesRec e = R.prec[r];
+        R.prec[r].gbase = gb;
+        gb += (unsigned long long)e.npush;
+        if (oracle) {
+            tot += e.d1;
+            if (e.inst < 0 && tot > pk) pk = tot;
+            tot += e.d2;
+        }
+    }
+    const long long ntot = s_pk[0], dtot = s_pk[1];
+    __syncthreads();
+    // CTA max of the sampled totals
+    for (int o = 16; o; o >>= 1) pk = max(pk, __shfl_xor_sync(FULL, pk, o));
+    if (lane_id() == 0) s_pk[tid >> 5] = pk;
+    __syncthreads();
+    if (tid == 0) {
+        long long m = ctl->peak;
+        for (int w = 0; w < (T >> 5); ++w) m = max(m, s_pk[w]);
+        ctl->peak = m;
+        ctl->gseq = G0 + (unsigned long long)ntot;
+        ctl->total = tot0 + dtot;
+    }
+    __syncthreads();
+    return true;
+}
+
+// Replace the provisional keys left in instance i's heap by the merged global
+// seqs (the relative order of the heap's keys is unchanged: provisional keys
+// follow every global one and keep their push order, so do their seqs).
+DEVI void pdes_fix_heap(const Rep& R, int i) {
+    HeapEnt* h = inst_heap(R, i);
+    const int hn = R.s.hn[i];
+    for (int k = 1 + lane_id(); k <= hn; k += 32) {
+        const unsigned long long key = h[k].key;
+        if ((key >> 29) & kPdesProv) h[k].key = pdes_global_key(R.prec, key);
+    }
 }
 
 template <bool TAIL_FAST>
@@ -154,7 +299,7 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
     const int ni = d.ni;
     // ---- shared-memory carve-up (engine.h pdes_smem)
     char* sp = smem;
-    R.s.gpu = reinterpret_cast<long long*>(sp);
+    R.s.gpu = reinterpret_cast<long long*>(sp + 32);  // rcp_of slots ahead
     R.s.cpu = R.s.gpu + max_ni;
     R.s.iter_start = reinterpret_cast<double*>(R.s.cpu + max_ni);
     R.s.link = R.s.iter_start + max_ni;
@@ -167,13 +312,16 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
     R.s.busy = R.s.blen + max_ni;
     R.s.healthy = R.s.busy + max_ni;
     sp += smem_inst_bytes(max_ni);
-    R.s.evseq = reinterpret_cast<unsigned long long*>(sp);
-    R.s.gtime = reinterpret_cast<double*>(R.s.evseq + max_ni);
-    R.s.hn = reinterpret_cast<int*>(R.s.gtime + max_ni);
+    R.s.gtime = reinterpret_cast<double*>(sp);
+    R.s.mt = R.s.gtime + max_ni;
+    R.s.mk = reinterpret_cast<unsigned long long*>(R.s.mt + max_ni);
+    R.s.hn = reinterpret_cast<int*>(R.s.mk + max_ni);
     R.s.hspill = R.s.hn + max_ni;
     R.s.enq = reinterpret_cast<unsigned*>(R.s.hspill + max_ni);
     R.s.dmin = reinterpret_cast<int*>(R.s.enq + max_ni);
-    sp += max_ni * 32;
+    R.s.mcur = R.s.dmin + max_ni;
+    R.s.mend = R.s.mcur + max_ni;
+    sp += max_ni * 48;
     R.s_heap = reinterpret_cast<HeapEnt*>(sp);
     sp += max_ni * hs * 16;
     char* wbase = sp;
@@ -184,11 +332,12 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
     R.s_tmp = R.s_cand + c_smem;
     R.s_tmpq = reinterpret_cast<unsigned*>(R.s_tmp + c_smem);
     R.s_cstat = reinterpret_cast<unsigned char*>(R.s_tmpq + c_smem);
-    R.prec = reinterpret_cast<PeakRec*>(wsp + smem_cand_bytes(c_smem));
-    const char* prec_all = wbase + smem_cand_bytes(c_smem);
-    const int prec_stride = wbytes;  // bytes between warps' record buffers
+    R.prec = a.prec + (long long)blockIdx.x * kPdesMaxWarps * kPdesRecCap;
+    R.pord = a.pord + (long long)blockIdx.x * kPdesMaxWarps * kPdesRecCap;
+    PdesRec* const myrec = R.prec + (long long)warp * kPdesRecCap;
     PdesCtl* ctl = reinterpret_cast<PdesCtl*>(wbase + W * wbytes);
 
+    if (threadIdx.x < 32) set_rcps(R);  // thread 0 writes
     for (int i = threadIdx.x; i < ni; i += blockDim.x) {
         R.s.gpu[i] = 0;
         R.s.cpu[i] = 0;
@@ -197,11 +346,12 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
         R.s.hi_len[i] = R.s.lo_len[i] = R.s.hcount[i] = R.s.lcount[i] = 0;
         R.s.afresh[i] = R.s.blen[i] = R.s.busy[i] = 0;
         R.s.healthy[i] = 1;
-        R.s.evseq[i] = 0;
         R.s.gtime[i] = CUDART_INF;
         R.s.hn[i] = R.s.hspill[i] = 0;
         R.s.enq[i] = 0;
         R.s.dmin[i] = 255;
+        R.s.mcur[i] = R.s.mend[i] = -1;
+        R.s.mk[i] = (unsigned long long)R.n;  // FCFS / RR: per-instance push seqs after the arrivals
     }
     for (int k = threadIdx.x; k < R.n; k += blockDim.x) {  // engine.cpp:382-389
         ReqState z0;
@@ -225,6 +375,7 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
     }
     if (threadIdx.x == 0) {
         ctl->next_arr = 0;
+        ctl->gseq = (unsigned long long)R.n;  // arrivals hold seqs 1..n (engine.cpp:384-389)
         ctl->total = 0;
         ctl->peak = 0;
         for (int c = 0; c < 10; ++c) ctl->cnt[c] = 0;
@@ -249,13 +400,20 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
     S.events = S.plans = S.visits = S.req_iters = S.ans_tokens = S.health = 0;
     S.adm_rounds = S.adm_slow = 0;
     S.prec_base = 0;
-    S.prec_n = 0;
-    S.cur_inst = 0;
+    S.d1 = 0;
+    S.sampled = false;
+    S.rec_n = 0;
+    S.npush = 0;
+    S.gseq = 0;
     S.phase_b = false;
     S.reason = 0;
     S.nb = 0;
     const bool pascal = R.policy == kPascal;
     const bool oracle = R.policy == kOracle;
+    // exact global seqs (records + merge) where cross-instance order matters:
+    // Pascal (boundaries read every instance) and the oracle (Σ gpu_used
+    // samples); FCFS / RR order per instance only (heap_push)
+    const bool exact = pascal || oracle;
     const double L = d.lookahead;
 
     long long rounds = 0;
@@ -266,22 +424,24 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
         // time a new cross-instance event could be created (Pascal: an
         // instance whose queued requests are >= d tokens from a phase
         // boundary cannot end one before its next event + max(1, d-1)
-        // iterations of >= lookahead each; the oracle bounds its rounds by
-        // one lookahead to bound its peak records)
+        // iterations of >= lookahead each, d capped so a round stays within
+        // the record buffers; the oracle bounds its rounds by one lookahead)
         double mn = CUDART_INF, gg = CUDART_INF, eb = CUDART_INF;
         for (int i = warp; i < ni; i += W) {
             if (R.s.hn[i] > 0) {
                 const double t = inst_heap(R, i)[1].t;
                 mn = fmin(mn, t);
                 if (pascal) {
-                    const int dk = max(1, R.s.dmin[i] - 1);
+                    const int dk = min(64, max(1, R.s.dmin[i] - 1));
                     // (1 - 1e-9) covers the rounding of dk repeated additions
                     eb = fmin(eb, __dadd_rn(t, __dmul_rn((double)dk * L, 1.0 - 1e-9)));
                 }
             }
             gg = fmin(gg, R.s.gtime[i]);
+            if (lane_id() == 0) R.s.mcur[i] = R.s.mend[i] = -1;
         }
-        if (oracle && mn < CUDART_INF && L > 0.0) eb = __dadd_rn(mn, L);
+        if (oracle && mn < CUDART_INF && L > 0.0)  // no boundaries: bound the round's size
+            eb = __dadd_rn(mn, __dmul_rn(64.0 * L, 1.0 - 1e-9));
         if (lane_id() == 0) {
             ctl->wmin[warp] = mn;
             ctl->wg[warp] = gg;
@@ -297,18 +457,13 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
             EB = fmin(EB, ctl->web[w]);
             if (st == 0) st = ctl->wstat[w];
         }
-        const int na = ctl->next_arr;
+        const int na0 = ctl->next_arr;
         __syncthreads();  // everyone has read the round-start state
         if (st != 0) break;
-        const double TA = na < R.n ? R.arrival[na] : CUDART_INF;
+        const double TA = na0 < R.n ? R.arrival[na0] : CUDART_INF;
         if (MN == CUDART_INF && TA == CUDART_INF) break;
         const double H = fmin(fmin(TA, G), EB);
-        // Phase B action (warp 0, after every warp finished phase A):
-        // 1 = the arrival at H, 2 = instance gi's cross-instance event at H
-        int bact = 0, gi = -1;
-        if (TA == H && TA <= G && TA < CUDART_INF) bact = 1;
-        else if (G == H && G < CUDART_INF) bact = 2;
-        if (bact == 0 && !(MN < H)) {  // no event can advance: decline
+        if (!(MN < H) && !(TA == H) && !(G == H)) {  // no event can advance: decline
             if (threadIdx.x == 0) {
                 ctl->status = kErrPdes;
                 ctl->reason = kPdesNoProgress;
@@ -319,16 +474,15 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
 
         // ---- one event loop (a single inlined copy of the handlers and the
         // planner) run in two passes: pass 0 = phase A (every warp, its own
-        // instances' events before H), pass 1 = phase B (warp 0: the event at
-        // H). The CTA barrier between the passes (one PC for every warp)
-        // orders every warp's phase-A shared-memory writes before warp 0's
-        // phase-B reads, and phase B's writes before the next round.
-        S.prec_n = 0;
+        // instances' events before H), pass 1 = phase B (warp 0: every event
+        // at H in (time, seq) order). CTA barriers between the phases order
+        // the shared-memory writes of one phase before the reads of the next.
+        S.rec_n = 0;
         int ii = warp;
-        bool b_started = false, b_over = false;
 #pragma unroll 1
         for (int pass = 0; pass < 2; ++pass) {
           S.phase_b = pass == 1;
+          if (S.phase_b) S.gseq = ctl->gseq;
           while (true) {
             HeapEnt e;
             int inst = -1;
@@ -336,48 +490,45 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
                 while (ii < ni && !(S.status == 0 && R.s.hn[ii] > 0 && inst_heap(R, ii)[1].t < H))
                     ii += W;
                 if (ii >= ni) break;
+                if (exact && S.rec_n >= kPdesRecCap) {
+                    if (S.status == 0) S.status = kErrPdes, S.reason = kPdesRecs;
+                    break;
+                }
                 inst = ii;
+                if (exact && lane_id() == 0 && R.s.mcur[ii] < 0)
+                    R.s.mcur[ii] = warp * kPdesRecCap + S.rec_n;
                 e = heap_pop_inst(R, ii);
             } else {
-                if (warp != 0 || bact == 0 || S.status != 0 || b_over) break;
-                if (bact == 1) {
-                    b_over = true;
-                    e.t = TA;
+                if (warp != 0 || S.status != 0) break;
+                // the next event at exactly H: the arrival (seq k + 1) or the
+                // heap top with the smallest global key
+                const int na = ctl->next_arr;
+                const bool arr = na < R.n && R.arrival[na] == H;
+                unsigned long long bk = ~0ull;
+                int bi = -1;
+                for (int i = lane_id(); i < ni; i += 32) {
+                    if (R.s.hn[i] > 0) {
+                        const HeapEnt top = inst_heap(R, i)[1];
+                        if (top.t == H && top.key < bk) bk = top.key, bi = i;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const unsigned long long k2 = __shfl_xor_sync(FULL, bk, o);
+                    const int i2 = __shfl_xor_sync(FULL, bi, o);
+                    if (k2 < bk) bk = k2, bi = i2;
+                }
+                if (arr && (bi < 0 || ((unsigned long long)na + 1) < (bk >> 29))) {
+                    e.t = H;
                     e.key = (unsigned long long)na;  // kind 0 = arrival
+                    __syncwarp();
                     if (lane_id() == 0) ctl->next_arr = na + 1;
+                    __syncwarp();
+                } else if (bi >= 0) {
+                    inst = bi;
+                    e = heap_pop_inst(R, bi);
                 } else {
-                    if (!b_started) {
-                        // the cross-instance event's instance; any other
-                        // instance with a pending event at exactly H (or a
-                        // second cross-instance event) would need the global
-                        // seq order: decline
-                        int cnt = 0, who = -1;
-                        for (int i = lane_id(); i < ni; i += 32) {
-                            if (R.s.gtime[i] == H) {
-                                ++cnt;
-                                who = i;
-                            } else if (R.s.hn[i] > 0 && inst_heap(R, i)[1].t == H) {
-                                ++cnt;
-                            }
-                        }
-                        cnt = warp_sum(cnt);
-                        who = (int)warp_max_u((unsigned)(who + 1)) - 1;
-                        b_started = true;
-                        if (cnt != 1 || who < 0) {
-                            if (S.status == 0) S.status = kErrPdes;
-                            if (lane_id() == 0) atomicCAS(&ctl->reason, 0, kPdesTieB);
-                            break;
-                        }
-                        gi = who;
-                    }
-                    if (R.s.hn[gi] == 0) {  // cannot happen: the event is pending
-                        if (S.status == 0) S.status = kErrPdes;
-                        break;
-                    }
-                    inst = gi;
-                    e = heap_pop_inst(R, gi);
-                    const unsigned k = (unsigned)(e.key >> 26) & 7u;
-                    if (k == EV_ITER || k == EV_PREFILL) b_over = true;
+                    break;
                 }
             }
             // ---- process one event (engine.cpp:392-404 loop body)
@@ -385,6 +536,9 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
             const unsigned id = (unsigned)(e.key & ((1u << 26) - 1u));
             S.events++;
             S.now = e.t;  // an instance's events pop in (time, seq) order
+            S.npush = 0;
+            S.sampled = false;
+            S.prec_base = S.gpu_total;
             if (kind == EV_ITER || kind == EV_PREFILL) {
                 if (lane_id() == 0) R.s.gtime[inst] = CUDART_INF;
                 __syncwarp();
@@ -399,30 +553,56 @@ DEVI void run_replica_pdes(const Arena& a, int r, char* smem, int max_ni, int hs
                 case EV_SWAP: plan_inst = on_swap_complete(R, S, (int)id); break;
                 default: plan_inst = on_transfer_complete(R, S, (int)id); break;
             }
-            S.cur_inst = plan_inst;
-            if (S.phase_b) S.nb++;
             maybe_start<TAIL_FAST>(R, S, plan_inst);
-            if (oracle) peak_record(R, S, false);
+            // the event's changes of Σ gpu_used before / after its sample
+            const long long dt = S.gpu_total - S.prec_base;
+            const long long d1 = S.sampled ? S.d1 : dt;
+            const long long d2 = dt - d1;
+            if (!S.phase_b) {
+                if (exact && lane_id() == 0) {
+                    PdesRec rc;
+                    rc.t = e.t;
+                    rc.key = e.key;
+                    rc.d1 = d1;
+                    rc.d2 = d2;
+                    rc.inst = inst | (S.sampled ? (int)0x80000000u : 0);
+                    rc.npush = S.npush;
+                    rc.gbase = 0;
+                    rc.rank = 0;
+                    rc.pad = 0;
+                    myrec[S.rec_n] = rc;
+                    R.s.mend[inst] = warp * kPdesRecCap + S.rec_n + 1;
+                }
+                S.rec_n++;
+                __syncwarp();
+            } else {
+                S.nb++;
+                if (oracle && lane_id() == 0) {  // serial: the exact global order
+                    long long tot = ctl->total + d1;
+                    if (S.sampled && tot > ctl->peak) ctl->peak = tot;
+                    ctl->total = tot + d2;
+                }
+                __syncwarp();
+            }
             if (S.status != 0 && !S.phase_b && warp != 0) break;
           }
+          if (pass == 0 && lane_id() == 0) ctl->wrec[warp] = S.rec_n;
           __syncthreads();
+          if (pass == 0 && exact) {
+              // exact global seqs for the phase-A pushes, then the heaps
+              if (!pdes_merge_par(R, ctl, ni, W, oracle)) {  // a time tie: serial merge
+                  if (warp == 0) pdes_merge(R, ctl, ni, oracle);
+                  __syncthreads();
+              }
+              for (int i = warp; i < ni; i += W) pdes_fix_heap(R, i);
+              __syncthreads();
+          } else if (pass == 1 && warp == 0 && lane_id() == 0) {
+              ctl->gseq = S.gseq;
+          }
         }
         if (lane_id() == 0) {
-            ctl->wrec[warp] = S.prec_n;
             if (S.status != 0) atomicCAS(&ctl->status, 0, S.status);
             if (S.reason != 0) atomicCAS(&ctl->reason, 0, S.reason);
-        }
-        __syncthreads();
-        if (oracle) {
-            pdes_merge_peak(ctl, prec_all, prec_stride, W);
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                long long tot = ctl->total;
-                for (int w = 0; w < W; ++w)
-                    for (int j = 0; j < ctl->wrec[w]; ++j)
-                        tot += prec_at(prec_all, prec_stride, w, j).d;
-                ctl->total = tot;
-            }
         }
         __syncthreads();
     }

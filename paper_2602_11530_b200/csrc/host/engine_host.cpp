@@ -323,6 +323,8 @@ public:
     DevBuf<pb::ReplicaDesc> d_desc_, d_odesc_, d_desc_init_;
     DevBuf<pb::ReplicaOut> d_out_, d_oout_;
     DevBuf<int> d_work_, d_omap_, d_oref_, d_rid_, d_order_, d_oorder_, d_sub_;
+    DevBuf<pb::PdesRec> d_prec_;  // instance-parallel engine: per-CTA event records
+    DevBuf<int> d_pord_;          // and their merged order
     DevBuf<double> d_arrival_, d_frac_;
     DevBuf<int4> d_spec_, d_cand_, d_tmp_;
     DevBuf<pb::ReqState> d_rs_;
@@ -687,6 +689,8 @@ pb::Arena Batch::arena(bool oracle) const {
     a.elist = d_elist_.p;
     a.stack = d_stack_.p;
     a.log = d_log_.p;
+    a.prec = d_prec_.p;
+    a.pord = d_pord_.p;
     a.wstride = total_req_;
     return a;
 }
@@ -743,14 +747,20 @@ void Batch::execute() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        const int budget = std::max(48 * 1024, optin) - 1024;
+        // dynamic shared memory beside the kernel's static 4 KB merge scratch
+        const int budget = std::max(48 * 1024, optin) - 6 * 1024;
         int c = std::max(32, std::min(max_n, 512)), hs = 32;
         while (pb::pdes_smem(max_ni_, hs, c, pdes_w_) > budget && c > 32) c /= 2;
         while (pb::pdes_smem(max_ni_, hs, c, pdes_w_) > budget && hs > 4) hs /= 2;
+        const int blocks = std::min(reps, sms);
+        d_prec_.ensure((size_t)blocks * pb::kPdesMaxWarps * pb::kPdesRecCap);
+        d_pord_.ensure((size_t)blocks * pb::kPdesMaxWarps * pb::kPdesRecCap);
+        ar.prec = d_prec_.p;
+        ar.pord = d_pord_.p;
         PLauncher eng = pre_run ? (spec ? pb::pdes_oracle::launch_engine : pb::pdes::launch_engine)
                                 : (spec && common == pb::kPascal ? pb::pdes_pascal::launch_engine
                                                                  : pb::pdes::launch_engine);
-        if (eng(ar, max_ni_, hs, c, pdes_w_, std::min(reps, sms), st_))
+        if (eng(ar, max_ni_, hs, c, pdes_w_, blocks, st_))
             throw std::logic_error("instance-parallel engine launch failed");
         launches += 1;
         std::vector<pb::ReplicaOut> outs(reps);

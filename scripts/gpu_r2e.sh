@@ -1,0 +1,10 @@
+# exact-seq instance-parallel engine: parity, decline check, timings, sanitizers
+OUT=gpurun_out/r2e; mkdir -p $OUT
+PB_PDES_DEBUG=1 timeout 600 python scripts/pdes_check.py parity > $OUT/pdes_parity.txt 2>&1; echo "pdes parity exit $?"; grep -E "BAD|declined|parity:" $OUT/pdes_parity.txt | tail -8
+PB_PDES_DEBUG=1 timeout 900 python scripts/pdes_check.py time c2_pascal c3_l8_pascal c3_l8_nonadaptive c3_l16_pascal c3_l16_nonadaptive c3_l8_fcfs c4s_pascal c4s_fcfs > $OUT/pdes_times.txt 2>&1; grep -v "replica [1-9]" $OUT/pdes_times.txt | cut -c1-330
+timeout 1500 python -m pytest tests/test_parity_gpu.py -q -m gpu -k "xlarge or instance_parallel" > $OUT/pytest_xl.log 2>&1; echo "pytest xl exit $?"; tail -5 $OUT/pytest_xl.log
+CS=/usr/local/cuda/bin/compute-sanitizer
+for tool in racecheck synccheck memcheck; do
+  timeout 900 $CS --tool $tool --print-limit 10 --error-exitcode 9 python scripts/sanitize_cases.py > $OUT/san_${tool}.log 2>&1
+  echo "$tool exit $?"; tail -1 $OUT/san_${tool}.log
+done

@@ -16,7 +16,7 @@ rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[2]
 i_s = hdr.index("Warp Stall Sampling (All Samples)")
 i_i = hdr.index("Instructions Executed")
-src = open(os.path.join(ROOT, "paper_2602_11530_b200/csrc/engine.cu")).read().split("\n")
+src = open(sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "paper_2602_11530_b200/csrc/engine.cu")).read().split("\n")
 funcs = []
 for n, line in enumerate(src, 1):
     m = re.match(r"(?:DEVI|__global__|template <[^>]*>|int)\s+[\w:<>\*& ]*?(\w+)\(", line)

@@ -64,8 +64,13 @@ def test_large_bit_exact(c, tmp_path):
         assert sha_file(f"{prefix}.{ext}") == want, ext
 
 
+# (points whose reference run took over a minute — the C5 thrash rates under
+# Pascal — are simulated only with PB_SLOW=1; the driver's GPU test budget is
+# 20 minutes)
 XLARGE = [c for c in CASES if c["name"] in GOLD and c["size"] in ("xlarge", "thrash")
-          and "records" in GOLD[c["name"]]]
+          and "records" in GOLD[c["name"]]
+          and (c["size"] == "xlarge" or os.environ.get("PB_SLOW")
+               or (GOLD[c["name"]].get("ref_run_s") or 0) <= 60)]
 
 
 @pytest.mark.gpu
