@@ -55,6 +55,22 @@
 #if PB_PDES && PB_LOG
 #error "the instance-parallel engine has no decision-log build"
 #endif
+// PB_PARK (the lean Pascal build only): an instance "parks" the all-denied
+// tail of its class-1 candidates — requests on the CPU, not swapping, whose
+// admission need exceeds the free KV and who have no reachable victim — by
+// flagging their low-queue entries. Parked requests are frozen until a plan
+// admits them (nothing but a plan touches a CPU-resident, non-swapping
+// request), so later plans skip them — no request-state read, no ordering,
+// admission or apply work — as long as a check at their position in the
+// priority order proves they would all be denied again without side effects
+// (see maybe_start). Their blocked-time additions are logged per instance
+// and replayed, in the same order, when they are unparked. Results are
+// bit-identical to the reference; only the work changes.
+#if !PB_LOG && !PB_PDES && defined(PB_ONLY_POLICY) && PB_ONLY_POLICY == 3
+#define PB_PARK 1
+#else
+#define PB_PARK 0
+#endif
 
 namespace pb {
 namespace PB_VARIANT {
@@ -99,6 +115,7 @@ DEVI bool m_candidate(unsigned m) {
 
 // candidate flags (int4::w of the candidate scratch)
 constexpr int CF_LOW = 1, CF_WAIT = 2, CF_RES = 4, CF_QPOS = 8, CF_TNEXT = 16;
+constexpr int CF_POS_SHIFT = 5;  // PB_PARK: the candidate's queue position above the flags
 // candidate status
 constexpr unsigned char CS_ADMIT = 1, CS_DENY = 2;
 
@@ -112,26 +129,23 @@ DEVI unsigned lanemask_lt() {
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
 }
+// Sum of non-negative 64-bit lane values (KV token counts) below 2^63: three
+// independent 32-bit REDUX sums of 24 / 24 / 15-bit slices (none overflows
+// across 32 lanes).
 DEVI long long warp_sum_ll(long long v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
+    const unsigned long long u = (unsigned long long)v;
+    const unsigned lo = __reduce_add_sync(FULL, (unsigned)(u & 0xffffffu));
+    const unsigned mid = __reduce_add_sync(FULL, (unsigned)((u >> 24) & 0xffffffu));
+    const unsigned hi = __reduce_add_sync(FULL, (unsigned)(u >> 48));
+    return (long long)((unsigned long long)lo + ((unsigned long long)mid << 24) +
+                       ((unsigned long long)hi << 48));
 }
-DEVI int warp_sum(int v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
-}
-DEVI unsigned warp_min_u(unsigned v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
-    return v;
-}
-DEVI unsigned warp_max_u(unsigned v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
-    return v;
-}
+// 32-bit warp reductions: one REDUX instruction instead of a five-step
+// shuffle chain (the planner's per-plan reductions sit on the replica's
+// serial dependency chain)
+DEVI int warp_sum(int v) { return (int)__reduce_add_sync(FULL, (unsigned)v); }
+DEVI unsigned warp_min_u(unsigned v) { return __reduce_min_sync(FULL, v); }
+DEVI unsigned warp_max_u(unsigned v) { return __reduce_max_sync(FULL, v); }
 DEVI int warp_excl_scan(int v, int* total) {
     int x = v;
 #pragma unroll
@@ -199,6 +213,14 @@ struct Inst {  // shared-memory SoA for the replica's instances
     int* blen;
     int* busy;
     int* healthy;
+#if PB_PARK
+    // parked tail summary: members, min admission need, min priority key
+    // (quanta << 32 | seq), plans logged in plog since the first member parked
+    int* pcount;
+    int* pneed;
+    unsigned long long* pkey;  // 8-byte aligned: laid out ahead of the int arrays
+    int* plen;
+#endif
 #if PB_PDES
     // per-instance event heaps and sequence counters (instance-parallel engine)
     int* hn;                    // heap entries
@@ -253,6 +275,10 @@ struct Rep {
     unsigned* elist;
     unsigned* stack;
     LogEnt* log;
+#if PB_PARK
+    double* plog;  // this replica's per-instance plan-duration logs (kParkLog each)
+    int* pfrom;    // per request: plog index it joined the parked tail at
+#endif
     Inst s;
 #if PB_PDES
     HeapEnt* s_heap;  // per-instance shared-memory heap slots (hs each, 1-based)
@@ -475,6 +501,10 @@ DEVI HeapEnt heap_pop_inst(const Rep& R, int i) {
 #endif
 
 // ------------------------------------------------------------ queues
+// Parked low-queue entries carry kPark in their seq word (PB_PARK builds;
+// enqueue seqs stay below 2^31: <= 4 enqueues per request, < 2^26 requests).
+constexpr unsigned kPark = 0x80000000u;
+constexpr unsigned kSeqMask = PB_PARK ? 0x7fffffffu : 0xffffffffu;
 // Queue (instance i, class low) is an append-only array of {idx, seq}; an
 // entry is live iff hot[idx].seq == seq (dequeue zeroes the request's seq).
 // Live entries keep ascending-seq order, i.e. the order of the reference's
@@ -487,7 +517,7 @@ __device__ __noinline__ int queue_compact_impl(uint2* q, int len, const ReqState
         uint2 e = make_uint2(0, 0);
         if (k < len) {
             e = q[k];
-            live = (unsigned)rs[e.x].h.z == e.y;
+            live = (unsigned)rs[e.x].h.z == (e.y & kSeqMask);
         }
         unsigned mk = __ballot_sync(FULL, live);
         __syncwarp();
@@ -649,7 +679,7 @@ DEVI bool instance_healthy(const HealthView& V, double now, int i, long long* ch
         if (k < len) {
             uint2 e = q[k];
             int4 h = V.rs[e.x].h;
-            if ((unsigned)h.z == e.y) {
+            if ((unsigned)h.z == (e.y & kSeqMask)) {
                 unsigned m = V.rs[e.x].meta;
                 if (m_phase(m) == PH_ANSWER) {
                     chk = true;
@@ -929,21 +959,37 @@ DEVI void pop_stack(const Rep& R, Adm& A, int s, long long need) {
     }
 }
 
+// Parked-tail bookkeeping of one plan (PB_PARK): the parked tail's min key
+// and what the low-queue gather measured against it (class-1 candidates
+// keyed below it).
+struct ParkG {
+    unsigned long long pkey;  // min (quanta << 32 | seq) over the parked tail
+    int below;                // class-1 candidates with key < pkey
+};
+DEVI unsigned long long prio_key(int4 h) {  // (quanta_exhausted, enqueue_seq)
+    return ((unsigned long long)(unsigned)h.w << 32) | (unsigned)h.z;
+}
+
 // Gather one queue (demoting first when Pascal scans the high queue) into
 // cand[nt..] in queue order; quanta go to tmpq for the partition. Returns the
 // min / max quanta of the gathered candidates, how many have quanta 0, the
 // highest position holding a resident KV footprint (-1 if none) and, when
 // `count_q`, the quanta histogram for the partition (lane b: quanta == b).
+// PB_PARK: a candidate's flags carry its queue position (bits 5..31); parked
+// low-queue entries are kept in place but not gathered.
 DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned& qmin,
                        unsigned& qmax, int& zero_q, int& rbpos, bool count_q, int& qcnt,
-                       unsigned& rem_min) {
+                       unsigned& rem_min, ParkG& pg) {
     unsigned lmin = 0xffffffffu, lmax = 0;
     unsigned lrem = 255u;  // PDES: min tokens to a phase boundary over the live entries
     int lzero = 0;
     int lrb = -1;
+    int lbelow = 0;
     uint2* q = queue_ptr(R, i, low);
     int len = low ? R.s.lo_len[i] : R.s.hi_len[i];
     const bool demote = (R.policy == kPascal) && !low;
+    // PB_PARK: parked entries whose request state is not read this pass
+    const bool skip_parked = PB_PARK && low;
     int w = 0;
     // Two-deep software pipeline: while chunk c is processed, the request
     // state of chunk c+1 and the queue entries of chunk c+2 are in flight.
@@ -955,8 +1001,10 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
     unsigned m_c = 0;
     if (ln < len) {
         e_c = q[ln];
-        h_c = R.rs[e_c.x].h;
-        m_c = R.rs[e_c.x].meta;
+        if (!(skip_parked && (e_c.y & kPark))) {
+            h_c = R.rs[e_c.x].h;
+            m_c = R.rs[e_c.x].meta;
+        }
     }
     if (32 + ln < len) e_n = q[32 + ln];
     for (int base = 0; base < len; base += 32) {
@@ -964,20 +1012,24 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
         int4 h_n = make_int4(0, 0, 0, 0);
         unsigned m_n = 0;
         uint2 e_nn = make_uint2(0, 0);
-        if (k + 32 < len) {
+        if (k + 32 < len && !(skip_parked && (e_n.y & kPark))) {
             h_n = R.rs[e_n.x].h;
             m_n = R.rs[e_n.x].meta;
         }
         if (k + 64 < len) e_nn = q[k + 64];
-        bool live = false, dem = false, cnd = false;
+        bool live = false, dem = false, cnd = false, parked = false;
         uint2 e = e_c;
         int4 h = h_c;
         unsigned m = 0;
         if (k < len) {
-            live = (unsigned)h.z == e.y;
-            if (live) {
-                m = m_c;
-                dem = demote && (long long)h.x > R.demotion;  // strict, instance.cpp:44
+            parked = skip_parked && (e.y & kPark);  // frozen: always live, never a candidate
+            live = parked;
+            if (!parked) {
+                live = (unsigned)h.z == e.y;
+                if (live) {
+                    m = m_c;
+                    dem = demote && (long long)h.x > R.demotion;  // strict, instance.cpp:44
+                }
             }
         }
         e_c = e_n;
@@ -1018,16 +1070,14 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
             __syncwarp();
         }
         bool keep = live && !dem;
-        cnd = keep && m_candidate(m);
+        cnd = keep && !parked && m_candidate(m);
         if (PB_PDES && live && (m_phase(m) == PH_WAIT || m_phase(m) == PH_REASON))
             lrem = min(lrem, m_rem(m));
         // compact the queue in place (tombstones and demoted entries leave)
         unsigned km = __ballot_sync(FULL, keep);
         __syncwarp();
-        {
-            const int dst = w + __popc(km & lanemask_lt());
-            if (keep && dst != k) q[dst] = e;  // entries only move past tombstones
-        }
+        const int qpos = w + __popc(km & lanemask_lt());
+        if (keep && qpos != k) q[qpos] = e;  // entries only move past tombstones
         w += __popc(km);
         // candidate record
         unsigned cm = __ballot_sync(FULL, cnd);
@@ -1047,6 +1097,10 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
             }
             if (h.w > 0) flags |= CF_QPOS;
             if (PB_PDES && m_tnext(m)) flags |= CF_TNEXT;
+            if (PB_PARK) {
+                flags |= qpos << CF_POS_SHIFT;
+                if (low) lbelow += prio_key(h) < pg.pkey;
+            }
             int pos = nt + __popc(cm & lanemask_lt());
             R.cand[pos] = make_int4((int)e.x, need, h.x, flags);
             R.tmpq[pos] = (unsigned)h.w;
@@ -1069,6 +1123,7 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
     qmin = warp_min_u(lmin);
     qmax = warp_max_u(lmax);
     if (PB_PDES) rem_min = min(rem_min, warp_min_u(lrem));
+    if (PB_PARK && low) pg.below = warp_sum(lbelow);
     zero_q = warp_sum(lzero);
     rbpos = (int)warp_max_u((unsigned)(lrb + 1)) - 1;
     __syncwarp();
@@ -1163,6 +1218,56 @@ DEVI int find_rb(const Rep& R, int b) {
     return -1;
 }
 
+#if PB_PARK
+// Unpark the members of instance i's parked tail whose admission need is at
+// most `thr` (LLONG_MAX: all): replay the plans they sat out (blocked += dur,
+// in plan order: the reference's own additions) and clear their flag; the
+// rest stay parked and the tail's summary is recomputed over them. With no
+// victim left at the tail's rank and the free KV there at `thr`, a member
+// needing more is denied wherever it ranks (free only shrinks past that
+// rank), so it may stay parked across the re-plan.
+DEVI void unpark(const Rep& R, int i, long long thr) {
+    uint2* q = queue_ptr(R, i, 1);
+    const int len = R.s.lo_len[i];
+    const double* lg = R.plog + (long long)i * kParkLog;
+    const int end = R.s.plen[i];
+    int cnt = 0;
+    unsigned mneed = 0xffffffffu;
+    unsigned long long mkey = ~0ull;
+    for (int k = lane_id(); k < len; k += 32) {
+        uint2 e = q[k];
+        if (!(e.y & kPark)) continue;
+        const int4 h = R.rs[e.x].h;
+        if ((long long)h.x + 1 <= thr) {
+            double b = R.blocked[e.x];
+            for (int p = R.pfrom[e.x]; p < end; ++p) b = __dadd_rn(b, lg[p]);
+            R.blocked[e.x] = b;
+            q[k].y = e.y & ~kPark;
+        } else {
+            ++cnt;
+            mneed = min(mneed, (unsigned)h.x + 1u);
+            const unsigned long long key = prio_key(h);
+            mkey = key < mkey ? key : mkey;
+        }
+    }
+    cnt = warp_sum(cnt);
+    mneed = warp_min_u(mneed);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(FULL, mkey, o);
+        mkey = y < mkey ? y : mkey;
+    }
+    __syncwarp();
+    if (lane_id() == 0) {
+        R.s.pcount[i] = cnt;
+        R.s.pneed[i] = cnt ? (int)mneed : INT_MAX;
+        R.s.pkey[i] = mkey;
+        if (!cnt) R.s.plen[i] = 0;
+    }
+    __syncwarp();
+}
+#endif
+
 // maybe_start (engine.cpp:192-258) with plan_iteration (instance.cpp:103-282).
 // TAIL_FAST: all-denied chunks (the swapped-out tail of an overloaded
 // instance) skip the per-chunk statistics and plan-application ballots. It
@@ -1187,6 +1292,28 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     }
     const bool pascal = R.policy == kPascal;
     const bool classed = pascal;
+    // PB_PARK: the instance's parked tail (pcnt members); a full duration log
+    // forces it back in
+    ParkG pg;
+    int pcnt = 0;
+#if PB_PARK
+    long long pthr = LLONG_MAX;  // unpark the members with need <= pthr
+    bool do_unpark = R.s.pcount[i] > 0 && R.s.plen[i] >= kParkLog;
+#endif
+    // PB_PARK: one pass when the parked tail is skipped (or there is none);
+    // when the check at its rank fails, the members it may concern are
+    // unparked and the plan is made again
+#pragma unroll 1
+    for (;;) {
+#if PB_PARK
+    if (do_unpark) unpark(R, i, pthr);  // one inlined copy for both sites
+    do_unpark = false;
+    pcnt = R.s.pcount[i];
+    pg.pkey = pcnt > 0 ? R.s.pkey[i] : ~0ull;
+#else
+    pg.pkey = ~0ull;
+#endif
+    pg.below = 0;
 
     // ---- gather (+ demotion) and priority order (instance.cpp:113-141)
     const bool by_quanta = R.policy == kRr || pascal;
@@ -1201,7 +1328,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         unsigned qmn, qmx;
         int zq, rbs, qc = 0;
         c1 = nt;
-        gather_queue(R, S, i, sg, nt, qmn, qmx, zq, rbs, by_quanta, qc, rem_min);
+        gather_queue(R, S, i, sg, nt, qmn, qmx, zq, rbs, by_quanta, qc, rem_min, pg);
         if (sg == 0) {
             qmin0 = qmn, qmax0 = qmx, z0 = zq, rb0 = rbs, qc0 = qc;
         } else {
@@ -1214,7 +1341,8 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     if (lane_id() == 0) R.s.dmin[i] = (int)rem_min;
 #endif
     const int n = nt;
-    S.visits += n;
+    // PB_PARK: skip the parked tail this plan (checked at its rank, `chk`)
+    const bool skip = PB_PARK && pcnt > 0;
     // priority order: the queue-ordered segments are partitioned into the
     // second scratch buffer, which then becomes the candidate array
     const bool part0 = by_quanta && qmin0 < qmax0;
@@ -1267,6 +1395,20 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     long long bcount = 0, bkv = 0;
     int nsw = 0, nimm = 0, nden = 0;
     bool tn_batch = false;  // PDES: a batch member's next token ends its reasoning
+    // PB_PARK: the parked tail ranks right before candidate `chk` (after the
+    // class-1 candidates keyed below it). It is denied again without side
+    // effects if, at that rank, something was admitted (no deadlock
+    // breaker), no class-1 resident is left to evict — none ranked after it
+    // but not yet evicted (rb < chk: every resident at or past b was evicted
+    // by an earlier admission's back walk) and none denied on the stack — and
+    // the free KV is below every member's need (with no victims left, free
+    // only shrinks past that rank).
+    int chk = skip ? c1 + pg.below : -1;
+    bool pfail = false;
+    // PB_PARK: the last position admitted, resident or class 0, and the last
+    // one that evicted: the denied, non-resident class-1 candidates after
+    // both are this plan's new parked members
+    int last_keep = -1, last_ev = -1;
     const int ln = lane_id();
     for (int base = 0; base < n; base += 32) {
         const int ci_l = base + ln;
@@ -1304,7 +1446,8 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
                     if (ln >= o) pin += y;
                 }
             }
-            const bool stop_here = (fc && (long long)pin > F) || (sf && !simple_sf);
+            const bool stop_here = (fc && (long long)pin > F) || (sf && !simple_sf) ||
+                                   (PB_PARK && mine && ci_l == chk);
             const unsigned sm = __ballot_sync(FULL, stop_here);
             const int stop = sm ? __ffs(sm) - 1 : cnt;
             const bool fin = mine && ln < stop;
@@ -1314,8 +1457,29 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             if (stop > 0) A.free_ -= taken;
             if (__ballot_sync(FULL, fin && fc)) any_admitted = true;
             if (stop >= cnt) break;
+#if PB_PARK
+            if (base + stop == chk) {  // the parked tail's rank
+                const bool novict = any_admitted && rb < chk && !(A.ns > 0 && stack_top >= c1);
+                if (!(novict && A.free_ < (long long)R.s.pneed[i])) {
+#ifdef PB_PARK_STATS
+                    S.adm_slow += !novict ? 1ll : 1ll << 16;
+#endif
+                    // with no victim left only members whose need fits the
+                    // free KV can be admitted; anything else: all come back
+                    pthr = novict ? A.free_ : LLONG_MAX;
+                    pfail = true;
+                    break;
+                }
+                chk = -1;
+                k = stop;
+                continue;
+            }
+            const int ne0 = A.ne;
+#endif
             // ---- exact reference step for candidate `stop`
+#ifndef PB_PARK_STATS
             S.adm_slow++;
+#endif
             const int ci = base + stop;
             const long long need = __shfl_sync(FULL, my_need, stop);
             const int cw = __shfl_sync(FULL, my_w, stop);
@@ -1349,8 +1513,21 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             stack_top = A.ns > 0 ? (int)R.stack[A.ns - 1] : -1;
             if (A.b != b0) rb = find_rb(R, A.b);
             if (ln == stop) st = dec;
+#if PB_PARK
+            if (A.ne != ne0) last_ev = ci;
+#endif
             k = stop + 1;
         }
+#if PB_PARK
+        if (pfail) break;
+        {
+            // (residents at or past b were evicted: they sit this plan out)
+            const unsigned km = __ballot_sync(
+                FULL, valid && (st == CS_ADMIT || ci_l < c1 ||
+                                ((my_w & CF_RES) && !(ci_l >= A.b && my_rkv > 0))));
+            if (km) last_keep = base + 31 - __clz(km);
+        }
+#endif
         if (valid) R.cstat[ci_l] = st;
         // statistics for this (now final) chunk
         const bool adm = st == CS_ADMIT, den = st == CS_DENY;
@@ -1375,6 +1552,26 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         nden += __popc(__ballot_sync(FULL, den));
         __syncwarp();
     }
+#if PB_PARK
+    if (chk == n) {
+        const bool novict = any_admitted && !(A.ns > 0 && stack_top >= c1);
+        if (!(novict && A.free_ < (long long)R.s.pneed[i])) {
+#ifdef PB_PARK_STATS
+            S.adm_slow += !novict ? 1ll : 1ll << 16;
+#endif
+            pthr = novict ? A.free_ : LLONG_MAX;
+            pfail = true;
+        }
+    }
+    if (pfail) {  // re-plan with (some of) the parked tail back in the queue
+        do_unpark = true;
+        continue;
+    }
+#ifdef PB_PARK_STATS
+    if (skip) S.adm_rounds += pcnt, S.adm_slow += 1ll << 48;
+#endif
+#endif
+    S.visits += n + (skip ? pcnt : 0);
     bkv = warp_sum_ll(bkv);
     if (A.free_ < 0) pop_stack(R, A, 0, 0);  // over-capacity repair :235-243
 
@@ -1430,6 +1627,24 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     int bpos = 0;
     long long mv = 0;
     unsigned* bout = R.batch + (long long)i * R.n;
+#if PB_PARK
+    // the skipped tail sat this plan out: log its blocked-time addition; the
+    // denied non-resident class-1 candidates after the last admitted /
+    // resident / evicting position join the tail (replaying from here on)
+    const int ptail = any_admitted ? max(max(last_keep, last_ev), c1 - 1) + 1 : n;
+    int pjoin = 0;
+    if (skip || ptail < n) {
+        pjoin = skip ? R.s.plen[i] : 0;  // a new tail starts an empty log
+        __syncwarp();
+        if (skip) {
+            if (lane_id() == 0) R.plog[(long long)i * kParkLog + pjoin] = dur;
+            ++pjoin;
+        }
+        if (lane_id() == 0) R.s.plen[i] = pjoin;
+    }
+    uint2* const qlow = queue_ptr(R, i, 1);
+    int pmin_need = INT_MAX, pfirst = INT_MAX, pnew = 0;
+#endif
     // pipelined: the blocked totals of the next chunk's denials are loaded
     // while this chunk is applied (a request is a candidate at most once)
     int4 c_n = make_int4(0, 0, 0, 0);
@@ -1455,6 +1670,17 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
             adm = st_c == CS_ADMIT;
             den = st_c == CS_DENY;
         }
+#if PB_PARK
+        // park: flag the queue entry, note the log index (residents past
+        // ptail were evicted: they are swapping out, not frozen)
+        if (k >= ptail && k < n && !(c.w & CF_RES)) {
+            qlow[(unsigned)c.w >> CF_POS_SHIFT].y |= kPark;
+            R.pfrom[c.x] = pjoin;
+            pmin_need = min(pmin_need, c.y);
+            pfirst = min(pfirst, k);
+            ++pnew;
+        }
+#endif
         if (TAIL_FAST && !logging && !__ballot_sync(FULL, adm)) {  // blocked time only
             if (den) R.blocked[c.x] = __dadd_rn(bl, dur);
             continue;
@@ -1507,6 +1733,23 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         }
     }
     S.nlog = log0 + A.ne + nsw + nimm + nden;
+#if PB_PARK
+    pnew = warp_sum(pnew);
+    if (pnew > 0) {
+        pmin_need = (int)warp_min_u((unsigned)pmin_need);
+        pfirst = (int)warp_min_u((unsigned)pfirst);
+        // the first new member has the lowest new key (priority order)
+        const unsigned long long k_new = prio_key(R.rs[R.cand[pfirst].x].h);
+        __syncwarp();
+        if (lane_id() == 0) {
+            R.s.pcount[i] = pcnt + pnew;
+            R.s.pneed[i] = min(skip ? R.s.pneed[i] : INT_MAX, pmin_need);
+            const unsigned long long k_old = skip ? R.s.pkey[i] : ~0ull;
+            R.s.pkey[i] = k_new < k_old ? k_new : k_old;
+        }
+        __syncwarp();
+    }
+#endif
     mv = warp_sum_ll(mv);
     add_cpu(R, i, -mv);
     add_gpu(R, S, i, mv);
@@ -1548,6 +1791,8 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
     __syncwarp();
     if (R.s.gpu[i] > R.cap && S.status == 0) S.status = kErrCapacity;
     note_peak(R, S);
+    break;
+    }  // PB_PARK re-plan loop
 }
 
 // --------------------------------------------------------------- events
@@ -1867,7 +2112,12 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     R.s.cpu = R.s.gpu + ni;
     R.s.iter_start = reinterpret_cast<double*>(R.s.cpu + ni);
     R.s.link = R.s.iter_start + ni;
+#if PB_PARK
+    R.s.pkey = reinterpret_cast<unsigned long long*>(R.s.link + ni);
+    R.s.hi_len = reinterpret_cast<int*>(R.s.pkey + ni);
+#else
     R.s.hi_len = reinterpret_cast<int*>(R.s.link + ni);
+#endif
     R.s.lo_len = R.s.hi_len + ni;
     R.s.hcount = R.s.lo_len + ni;
     R.s.lcount = R.s.hcount + ni;
@@ -1875,6 +2125,13 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
     R.s.blen = R.s.afresh + ni;
     R.s.busy = R.s.blen + ni;
     R.s.healthy = R.s.busy + ni;
+#if PB_PARK
+    R.s.pcount = R.s.healthy + ni;
+    R.s.pneed = R.s.pcount + ni;
+    R.s.plen = R.s.pneed + ni;
+    R.plog = a.plog + d.plog_base;
+    R.pfrom = a.pfrom + g;
+#endif
     sp += smem_inst_bytes(max_ni);
     const bool resident = R.n <= n_smem;  // request state in shared memory
     if (resident) {
@@ -1910,6 +2167,12 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
         R.s.hi_len[i] = R.s.lo_len[i] = R.s.hcount[i] = R.s.lcount[i] = 0;
         R.s.afresh[i] = R.s.blen[i] = R.s.busy[i] = 0;
         R.s.healthy[i] = 1;
+#if PB_PARK
+        R.s.pcount[i] = 0;
+        R.s.pneed[i] = INT_MAX;
+        R.s.plen[i] = 0;
+        R.s.pkey[i] = ~0ull;
+#endif
     }
     // reset per-request state (Simulator::run, engine.cpp:382-389)
     for (int k = lane_id(); k < R.n; k += 32) {

@@ -52,6 +52,7 @@ struct ReplicaDesc {
     long long batch_base;  // into batch: ni * n entries
     long long heap_base;   // into heap: n + ni + 2 entries
     long long log_base, log_cap;
+    long long plog_base;   // into plog: ni * kParkLog entries (lean Pascal build, parked tails)
     // instance-parallel (PDES) engine only
     long long pheap_base;  // into heap: ni * (n + 2) entries (per-instance heaps)
     double lookahead;      // lower bound on the duration of an event that can create a
@@ -166,6 +167,10 @@ struct Arena {
     unsigned* elist;
     unsigned* stack;
     LogEnt* log;
+    // lean Pascal build: durations of the plans that skipped an instance's parked
+    // tail (kParkLog per instance) and the log index each parked request joined at
+    double* plog;
+    int* pfrom;
     struct PdesRec* prec;  // PDES: kPdesMaxWarps * kPdesRecCap records per CTA
     int* pord;             // PDES: the same count of ints per CTA (records by rank)
     long long wstride;  // PDES: per-warp scratch copies (cand / tmp / tmpq / cstat / elist /
@@ -218,7 +223,11 @@ struct RowArrays {
 // HBM; plans with more queued requests than c_smem use the HBM scratch.
 // (+32: the replica's fixed-divisor reciprocals, engine.cu rcp_of, ahead of
 // the instance arrays)
-PB_HD inline int smem_inst_bytes(int ni) { return ((ni * 64 + 16 + 32) + 15) / 16 * 16; }
+// (+20 per instance: the parked-tail summary of the lean Pascal build, engine.cu PB_PARK)
+PB_HD inline int smem_inst_bytes(int ni) { return ((ni * 84 + 16 + 32) + 15) / 16 * 16; }
+// Parked tails (engine.cu PB_PARK): plans an instance may skip its parked
+// requests in before they are materialised.
+constexpr int kParkLog = 1024;
 PB_HD inline int smem_req_bytes(int n_smem) { return (n_smem * 60 + 15) / 16 * 16; }  // rs 32 + spec 16 + blocked 8 + aoff 4
 // Shared-memory event heap: sized for every pending event of a resident
 // replica; HBM-resident replicas start with h_slots slots (default 128) and

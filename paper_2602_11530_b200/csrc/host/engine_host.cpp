@@ -331,7 +331,8 @@ public:
     DevBuf<long long> d_aoff_, d_biggest_, d_echo_, d_seg_;
     DevBuf<unsigned> d_batch_, d_tmpq_, d_elist_, d_stack_;
     DevBuf<int> d_aoff32_;
-    DevBuf<double> d_blocked_;
+    DevBuf<double> d_blocked_, d_plog_;
+    DevBuf<int> d_pfrom_;
     DevBuf<pb::RecOut> d_rec_;
     DevBuf<double> d_dig_, d_del_, d_bpv_;
     DevBuf<int> d_bpk_;
@@ -389,7 +390,7 @@ void Batch::build() {
     oref_.clear();
     orep_.clear();
     std::map<std::string, int> oracle_of;
-    long long rq = 0, ans = 0, q = 0, bt = 0, hp = 0, lg = 0;
+    long long rq = 0, ans = 0, q = 0, bt = 0, hp = 0, lg = 0, pl = 0;
     for (int r = 0; r < n_rep_; ++r) {
         const Job& j = jobs_[r];
         const long long n = (long long)j.trace->size();
@@ -414,6 +415,9 @@ void Batch::build() {
         d.heap_base = hp;
         d.pheap_base = 0;  // set below when the instance-parallel engine is used
         d.log_base = lg;
+        // parked-tail duration logs: read only by the lean Pascal build
+        d.plog_base = pl;
+        if (j.cfg.policy == pb::kPascal) pl += (long long)ni * pb::kParkLog;
         {
             // lookahead of the instance-parallel engine (engine_pdes.cuh): a
             // lower bound on the duration of any decode iteration
@@ -565,6 +569,8 @@ void Batch::build() {
     d_rs_.ensure(rq);
     d_aoff32_.ensure(rq);
     d_blocked_.ensure(rq);
+    d_pfrom_.ensure(rq);
+    d_plog_.ensure(std::max<long long>(pl, 1));
     d_rec_.ensure(rq);
     // per-warp planner scratch: one copy per warp of a replica under the
     // instance-parallel engine
@@ -689,6 +695,8 @@ pb::Arena Batch::arena(bool oracle) const {
     a.elist = d_elist_.p;
     a.stack = d_stack_.p;
     a.log = d_log_.p;
+    a.plog = d_plog_.p;
+    a.pfrom = d_pfrom_.p;
     a.prec = d_prec_.p;
     a.pord = d_pord_.p;
     a.wstride = total_req_;
