@@ -327,6 +327,13 @@ DEVI void set_rcps(const Rep& R) {
     }
 }
 
+// 32 ints of per-warp scratch after the shared candidate scratch (engine.h
+// smem_cand_bytes): the quanta histogram / bucket offsets of the partition
+DEVI int* warp_hist(const Rep& R) {
+    return reinterpret_cast<int*>(
+        reinterpret_cast<char*>(R.s_cand) + (R.c_smem * 37 + 15) / 16 * 16);
+}
+
 DEVI uint2* queue_ptr(const Rep& R, int i, int low) {
     return R.qent + (long long)(2 * i + low) * R.qcap;
 }
@@ -396,10 +403,11 @@ DEVI void heap_push(const Rep& R, Scal& S, double t, unsigned kind, unsigned id,
     __syncwarp();
 }
 #endif
-DEVI HeapEnt heap_pop_at(HeapEnt* h, int n) {
-    HeapEnt top;
+// Lane 0 removes the root (sift-down); `top` is returned to every lane by
+// shuffles. heap_drop_at: the same without the broadcast, for a caller that
+// has already read the root in all lanes.
+DEVI void heap_drop_at(HeapEnt* h, int n) {
     if (lane_id() == 0) {
-        top = h[1];
         HeapEnt last = h[n];
         int m = n - 1;
         int i = 1;
@@ -420,16 +428,20 @@ DEVI HeapEnt heap_pop_at(HeapEnt* h, int n) {
         }
         if (m >= 1) h[i] = last;
     }
+}
+DEVI HeapEnt heap_pop_at(HeapEnt* h, int n) {
+    HeapEnt top;
+    if (lane_id() == 0) top = h[1];
+    heap_drop_at(h, n);
     top.t = __shfl_sync(FULL, top.t, 0);
     top.key = __shfl_sync(FULL, top.key, 0);
     return top;
 }
 #if !PB_PDES
-DEVI HeapEnt heap_pop(const Rep& R, Scal& S) {
-    HeapEnt top = heap_pop_at(S.heap, S.hn);
+DEVI void heap_pop(const Rep& R, Scal& S) {  // the caller read the root in every lane
+    heap_drop_at(S.heap, S.hn);
     S.hn = S.hn - 1;
     __syncwarp();
-    return top;
 }
 #else
 // Per-instance heaps: instance i's heap lives in its shared-memory slots
@@ -991,6 +1003,10 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
     // PB_PARK: parked entries whose request state is not read this pass
     const bool skip_parked = PB_PARK && low;
     int w = 0;
+    if (count_q) {
+        warp_hist(R)[lane_id()] = 0;
+        __syncwarp();
+    }
     // Two-deep software pipeline: while chunk c is processed, the request
     // state of chunk c+1 and the queue entries of chunk c+2 are in flight.
     // Safe because a request has at most one entry in a high queue (appended
@@ -1109,14 +1125,10 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
             lzero += h.w == 0;
             if ((flags & CF_RES) && h.x > 0) lrb = pos;  // positions grow per lane
         }
-        if (count_q) {  // one ballot per distinct quanta value in the chunk
-            unsigned todo = cm;
-            while (todo) {
-                const unsigned v = __shfl_sync(FULL, (unsigned)h.w, __ffs(todo) - 1);
-                const unsigned m = __ballot_sync(FULL, cnd && (unsigned)h.w == v);
-                if (ln == (int)v) qcnt += __popc(m);
-                todo &= ~m;
-            }
+        if (count_q) {  // quanta histogram: each value's lowest lane adds its peers
+            const unsigned pm = __match_any_sync(FULL, cnd ? (unsigned)h.w : 0xffffffffu);
+            if (cnd && (unsigned)h.w < 32u && !(pm & lanemask_lt()))
+                warp_hist(R)[h.w] += __popc(pm);
         }
         nt += __popc(cm);
     }
@@ -1124,6 +1136,10 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
     qmax = warp_max_u(lmax);
     if (PB_PDES) rem_min = min(rem_min, warp_min_u(lrem));
     if (PB_PARK && low) pg.below = warp_sum(lbelow);
+    if (count_q) {
+        __syncwarp();
+        qcnt = warp_hist(R)[lane_id()];
+    }
     zero_q = warp_sum(lzero);
     rbpos = (int)warp_max_u((unsigned)(lrb + 1)) - 1;
     __syncwarp();
@@ -1153,28 +1169,28 @@ DEVI int order_segment(const Rep& R, const int4* src, int4* dst, int s, int e, u
     const unsigned lt = lanemask_lt();
     int lrb = -1;
     if (qmax < 32) {
+        // bucket b's next slot lives in warp_hist[b]; per chunk, the lanes of
+        // one quanta value (match.any) take consecutive slots in lane order
+        int* off = warp_hist(R);
         int total;
-        int off = s + warp_excl_scan(qcnt, &total);  // lane b: first slot of bucket b
+        off[ln] = s + warp_excl_scan(qcnt, &total);  // lane b: first slot of bucket b
+        __syncwarp();
         for (int base = s; base < e; base += 32) {
             const int k = base + ln;
             const bool valid = k < e;
             const unsigned q = valid ? R.tmpq[k] : 0xffffffffu;
             const int4 v = valid ? src[k] : make_int4(0, 0, 0, 0);
-            unsigned todo = __ballot_sync(FULL, valid);
-            while (todo) {
-                const unsigned qv = __shfl_sync(FULL, q, __ffs(todo) - 1);
-                const unsigned m = __ballot_sync(FULL, q == qv);
-                const int o = __shfl_sync(FULL, off, qv);
-                if (q == qv) {
-                    const int d = o + __popc(m & lt);
-                    dst[d] = v;
-                    if (cand_rkv(v) > 0) lrb = max(lrb, d);
-                }
-                if (ln == (int)qv) off += __popc(m);
-                todo &= ~m;
+            const unsigned m = __match_any_sync(FULL, q);
+            const int o = valid ? off[q] : 0;
+            __syncwarp();
+            if (valid) {
+                const int d = o + __popc(m & lt);
+                dst[d] = v;
+                if (cand_rkv(v) > 0) lrb = max(lrb, d);
+                if (!(m & lt)) off[q] = o + __popc(m);
             }
+            __syncwarp();
         }
-        __syncwarp();
         return (int)warp_max_u((unsigned)(lrb + 1)) - 1;
     }
     int out = s;
@@ -1532,7 +1548,7 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         // statistics for this (now final) chunk
         const bool adm = st == CS_ADMIT, den = st == CS_DENY;
         if (TAIL_FAST && !__ballot_sync(FULL, adm)) {  // all-denied chunk
-            nden += __popc(__ballot_sync(FULL, den));
+            if (PB_LOG) nden += __popc(__ballot_sync(FULL, den));
             continue;
         }
         bool wt = false, inb = false, sw = false, imm = false;
@@ -1547,9 +1563,11 @@ DEVI void maybe_start(Rep& R, Scal& S, int i) {
         bcount += __popc(__ballot_sync(FULL, inb));
         if (PB_PDES && __ballot_sync(FULL, inb && (my_w & CF_TNEXT))) tn_batch = true;
         bkv += inb ? (long long)my.z : 0;  // lane-local; reduced after the loop
-        nsw += __popc(__ballot_sync(FULL, sw));
-        nimm += __popc(__ballot_sync(FULL, imm));
-        nden += __popc(__ballot_sync(FULL, den));
+        if (PB_LOG) {  // log-line positions only
+            nsw += __popc(__ballot_sync(FULL, sw));
+            nimm += __popc(__ballot_sync(FULL, imm));
+            nden += __popc(__ballot_sync(FULL, den));
+        }
         __syncwarp();
     }
 #if PB_PARK
@@ -2239,10 +2257,10 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
             id = (unsigned)S.next_arr++;
             if (S.next_arr < R.n) ta_next = R.arrival[S.next_arr];
         } else {
-            HeapEnt e = heap_pop(R, S);
-            et = e.t;
-            kind = (unsigned)(e.key >> 26) & 7u;
-            id = (unsigned)(e.key & ((1u << 26) - 1u));
+            heap_pop(R, S);  // top: the root every lane read above
+            et = top.t;
+            kind = (unsigned)(top.key >> 26) & 7u;
+            id = (unsigned)(top.key & ((1u << 26) - 1u));
         }
         S.events++;
         if (et < S.now - 1e-12) {
@@ -2273,7 +2291,7 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
         o.status = S.status;
         o.pad = 0;
         o.peak = S.peak;
-        o.nlog = S.nlog;
+        o.nlog = PB_LOG ? S.nlog : 0;  // log-free builds never size a log
         o.events = S.events;
         o.plans = S.plans;
         o.visits = S.visits;

@@ -236,7 +236,9 @@ constexpr int kSmemHeapSlots = 128;
 PB_HD inline int smem_heap_bytes(int n_smem, int ni, int h_slots = kSmemHeapSlots) {
     return n_smem ? (n_smem + ni + 2) * 16 : h_slots * 16;
 }
-PB_HD inline int smem_cand_bytes(int c_smem) { return (c_smem * 37 + 15) / 16 * 16; }
+// (+ 32 ints of per-warp bucket scratch for the planner's quanta partition,
+// engine.cu warp_hist)
+PB_HD inline int smem_cand_bytes(int c_smem) { return (c_smem * 37 + 15) / 16 * 16 + 128; }
 // HBM-resident replicas with n <= b_smem keep their blocked-time totals (the
 // most frequently written per-request value: one read-modify-write per denial)
 // in shared memory.
