@@ -338,6 +338,17 @@ DEVI uint2* queue_ptr(const Rep& R, int i, int low) {
     return R.qent + (long long)(2 * i + low) * R.qcap;
 }
 
+// First 64 entries of instance i's high and low queues into L1 (lanes 0..9:
+// five 128-byte lines per queue), ahead of the plan's dependent
+// queue-entry -> request-state loads.
+DEVI void prefetch_queue_heads(const Rep& R, int i) {
+    const int ln = lane_id();
+    if (ln < 10) {
+        const uint2* p = queue_ptr(R, i, ln >= 5) + (ln % 5) * 16;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+    }
+}
+
 // ------------------------------------------------------------- event log
 // Cold paths live out of line (__noinline__): the kernel's hot loop must stay
 // small for the instruction cache (L1.5 I$ is 32 KB per SM; the fully inlined
@@ -2272,7 +2283,12 @@ DEVI void run_replica(const Arena& a, int r, char* smem, int max_ni, int n_smem,
         switch (kind) {
             case 0: plan_inst = on_arrival(R, S, (int)id); break;
             case EV_PREFILL: plan_inst = on_prefill_complete(R, S, (int)id); break;
-            case EV_ITER: plan_inst = on_iteration_complete(R, S, (int)id); break;
+            case EV_ITER:
+                // the plan that follows gathers this instance's queues: pull
+                // their heads into L1 while the batch retires
+                prefetch_queue_heads(R, (int)id);
+                plan_inst = on_iteration_complete(R, S, (int)id);
+                break;
             case EV_SWAP: plan_inst = on_swap_complete(R, S, (int)id); break;
             default: plan_inst = on_transfer_complete(R, S, (int)id); break;
         }

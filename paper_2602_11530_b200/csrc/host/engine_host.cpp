@@ -20,6 +20,7 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <unordered_map>
 
 #include "common.hpp"
@@ -369,6 +370,26 @@ Batch::~Batch() {
     if (st_) cudaStreamDestroy(st_);
 }
 
+// Host staging of a batch touches every request a few times (lookahead,
+// footprint bounds, costs, the upload arrays): one pass per replica, run over
+// the host cores (replicas are independent; results land in per-replica
+// slots or disjoint ranges).
+template <class F>
+void parallel_replicas(int n, F fn) {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int nt = (int)std::min<long long>(hw, std::max(1, n / 64));
+    if (nt <= 1) {
+        for (int r = 0; r < n; ++r) fn(r);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            for (int r = t; r < n; r += nt) fn(r);
+        });
+    for (auto& x : th) x.join();
+}
+
 void Batch::build() {
     if (built_) return;
     built_ = true;
@@ -391,6 +412,23 @@ void Batch::build() {
     orep_.clear();
     std::map<std::string, int> oracle_of;
     long long rq = 0, ans = 0, q = 0, bt = 0, hp = 0, lg = 0, pl = 0;
+    // per-replica scans of the trace (parallel): the shortest prompt of an
+    // R = 0, not preloaded, A > 1 request (lookahead), the largest footprint,
+    // the answer tokens and the request-iterations (hand-out cost)
+    std::vector<long long> r_pmin(n_rep_), r_big(n_rep_), r_ans(n_rep_), r_iters(n_rep_);
+    parallel_replicas(n_rep_, [&](int r) {
+        long long pmin = -1, big = 0, a = 0;
+        for (const Spec& s : *jobs_[r].trace) {
+            if (s.reasoning == 0 && !s.preloaded && s.answering > 1)
+                pmin = pmin < 0 ? s.prompt : std::min<long long>(pmin, s.prompt);
+            big = std::max(big, (long long)s.max_kv());
+            a += s.answering;
+        }
+        r_pmin[r] = pmin;
+        r_big[r] = big;
+        r_ans[r] = a;
+        r_iters[r] = (long long)request_iterations(*jobs_[r].trace);
+    });
     for (int r = 0; r < n_rep_; ++r) {
         const Job& j = jobs_[r];
         const long long n = (long long)j.trace->size();
@@ -425,17 +463,13 @@ void Batch::build() {
             // B >= 1, K >= 0; rounding is monotone) and of any prefill that
             // ends in a phase boundary (R = 0, not preloaded, A > 1).
             double la = j.prof.decode_base + j.prof.decode_per_request * 1.0;
-            long long pmin = -1;
-            for (const Spec& s : *j.trace)
-                if (s.reasoning == 0 && !s.preloaded && s.answering > 1)
-                    pmin = pmin < 0 ? s.prompt : std::min<long long>(pmin, s.prompt);
+            const long long pmin = r_pmin[r];
             if (pmin >= 0)
                 la = std::min(la, j.prof.prefill_base + j.prof.prefill_per_token * (double)pmin);
             d.lookahead = la;
         }
         d.log_cap = log_cap_;
-        long long big = 0;
-        for (const Spec& s : *j.trace) big = std::max(big, (long long)s.max_kv());
+        const long long big = r_big[r];
         biggest[r] = big;
         frac[r] = j.cfg.capacity_fraction;
         const long long kOracleCap = LONG_MAX / 4;
@@ -484,7 +518,8 @@ void Batch::build() {
         max_n_ = std::max<int>(max_n_, (int)n);
         if (j.cfg.gpu_capacity <= 0) max_on_ = std::max<int>(max_on_, (int)n);
         rq += n;
-        for (const Spec& s : *j.trace) ans += s.answering;
+        if (r_ans[r] > INT_MAX) throw std::invalid_argument("replica answer tokens exceed 2^31");
+        ans += r_ans[r];
         q += 2ll * ni * (n + 1);
         bt += (long long)ni * std::max<long long>(n, 1);
         hp += n + ni + 2;
@@ -532,25 +567,31 @@ void Batch::build() {
     total_heap_ = hp;
     total_log_ = lg;
 
-    // ---- host staging of the read-only trace
-    std::vector<double> arrival(rq);
-    std::vector<int4> spec(rq);
-    std::vector<long long> aoff(rq);
-    std::vector<int> aoff32(rq);
-    std::vector<int> rid(rq);
-    long long g = 0, a = 0;
-    for (int r = 0; r < n_rep_; ++r) {
-        const long long a0 = a;
-        for (const Spec& s : *jobs_[r].trace) {
-            arrival[g] = s.arrival;
-            spec[g] = make_int4((int)s.prompt, (int)s.reasoning, (int)s.answering, s.preloaded ? 1 : 0);
-            aoff[g] = a;
-            if (a - a0 > INT_MAX) throw std::invalid_argument("replica answer tokens exceed 2^31");
-            aoff32[g] = (int)(a - a0);
-            rid[g] = r;
-            a += s.answering;
-            ++g;
-        }
+    // ---- host staging of the read-only trace (replicas in parallel, each
+    // into its own request range; arrays left uninitialised: every slot is
+    // written)
+    std::unique_ptr<double[]> arrival(new double[std::max<long long>(rq, 1)]);
+    std::unique_ptr<int4[]> spec(new int4[std::max<long long>(rq, 1)]);
+    std::unique_ptr<long long[]> aoff(new long long[std::max<long long>(rq, 1)]);
+    std::unique_ptr<int[]> aoff32(new int[std::max<long long>(rq, 1)]);
+    std::unique_ptr<int[]> rid(new int[std::max<long long>(rq, 1)]);
+    {
+        std::vector<long long> abase(n_rep_ + 1, 0);
+        for (int r = 0; r < n_rep_; ++r) abase[r + 1] = abase[r] + r_ans[r];
+        parallel_replicas(n_rep_, [&](int r) {
+            long long g = seg[r], a = abase[r];
+            const long long a0 = a;
+            for (const Spec& s : *jobs_[r].trace) {
+                arrival[g] = s.arrival;
+                spec[g] = make_int4((int)s.prompt, (int)s.reasoning, (int)s.answering,
+                                    s.preloaded ? 1 : 0);
+                aoff[g] = a;
+                aoff32[g] = (int)(a - a0);
+                rid[g] = r;
+                a += s.answering;
+                ++g;
+            }
+        });
     }
 
     // ---- device arenas
@@ -631,7 +672,7 @@ void Batch::build() {
     // for the queue-scanning policies.
     {
         auto cost = [&](int r) {
-            double c = (double)request_iterations(*jobs_[r].trace);
+            double c = (double)r_iters[r];
             return jobs_[r].cfg.policy == pb::kPascal || jobs_[r].cfg.policy == pb::kRr ? 2 * c : c;
         };
         std::vector<double> cr(n_rep_);
@@ -648,11 +689,11 @@ void Batch::build() {
         up(d_order_.p, order_.data(), order_.size() * sizeof(int));
         up(d_oorder_.p, oorder_.data(), oorder_.size() * sizeof(int));
     }
-    up(d_arrival_.p, arrival.data(), arrival.size() * sizeof(double));
-    up(d_spec_.p, spec.data(), spec.size() * sizeof(int4));
-    up(d_aoff_.p, aoff.data(), aoff.size() * sizeof(long long));
-    up(d_aoff32_.p, aoff32.data(), aoff32.size() * sizeof(int));
-    up(d_rid_.p, rid.data(), rid.size() * sizeof(int));
+    up(d_arrival_.p, arrival.get(), rq * sizeof(double));
+    up(d_spec_.p, spec.get(), rq * sizeof(int4));
+    up(d_aoff_.p, aoff.get(), rq * sizeof(long long));
+    up(d_aoff32_.p, aoff32.get(), rq * sizeof(int));
+    up(d_rid_.p, rid.get(), rq * sizeof(int));
     up(d_params_.p, params.data(), params.size() * sizeof(pb::MetricParams));
     up(d_frac_.p, frac.data(), frac.size() * sizeof(double));
     up(d_biggest_.p, biggest.data(), biggest.size() * sizeof(long long));
