@@ -20,6 +20,7 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <exception>
 #include <thread>
 #include <unordered_map>
 
@@ -355,21 +356,6 @@ public:
     pb::Arena arena(bool oracle) const;
 };
 
-Batch::Batch(const std::vector<Job>& jobs) : jobs_(jobs) {
-    for (const Job& j : jobs_) {
-        check_trace(*j.trace);
-        check_profile(j.prof);
-        check_limits(j);
-    }
-}
-
-Batch::~Batch() {
-    ScopedDevice sd(dev_);
-    for (auto& e : ev_)
-        if (e) cudaEventDestroy(e);
-    if (st_) cudaStreamDestroy(st_);
-}
-
 // Host staging of a batch touches every request a few times (lookahead,
 // footprint bounds, costs, the upload arrays): one pass per replica, run over
 // the host cores (replicas are independent; results land in per-replica
@@ -388,6 +374,31 @@ void parallel_replicas(int n, F fn) {
             for (int r = t; r < n; r += nt) fn(r);
         });
     for (auto& x : th) x.join();
+}
+
+Batch::Batch(const std::vector<Job>& jobs) : jobs_(jobs) {
+    // validation in parallel; the first failing replica's error is thrown,
+    // as the sequential loop would
+    std::vector<std::exception_ptr> err(jobs_.size());
+    parallel_replicas((int)jobs_.size(), [&](int r) {
+        try {
+            const Job& j = jobs_[r];
+            check_trace(*j.trace);
+            check_profile(j.prof);
+            check_limits(j);
+        } catch (...) {
+            err[r] = std::current_exception();
+        }
+    });
+    for (const auto& e : err)
+        if (e) std::rethrow_exception(e);
+}
+
+Batch::~Batch() {
+    ScopedDevice sd(dev_);
+    for (auto& e : ev_)
+        if (e) cudaEventDestroy(e);
+    if (st_) cudaStreamDestroy(st_);
 }
 
 void Batch::build() {
