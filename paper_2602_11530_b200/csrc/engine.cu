@@ -1065,7 +1065,7 @@ DEVI void gather_queue(const Rep& R, Scal& S, int i, int low, int& nt, unsigned&
         e_n = e_nn;
         // --- demotion (instance.cpp:39-57): new seqs in queue order, appended
         // to the low queue; logged "demote" in that order (engine.cpp:196-197).
-        unsigned dm = __ballot_sync(FULL, dem);
+        unsigned dm = demote ? __ballot_sync(FULL, dem) : 0u;  // (low queues never demote)
         if (dm) {
             int nd = __popc(dm);
             int lo_len = R.s.lo_len[i];
