@@ -69,8 +69,11 @@ C5_IDS = [r for r in range(4096 * 64) if sweep.replica_params(r)[1] >= 3]
 
 WORKLOADS = {
     # label: (description, default replicas per GPU)
+    # C2: eight replicas per resident warp (8 warps/SM x 148 SMs); the
+    # work-stealing loop's end-of-step tail is amortised over twice as many
+    # replicas as at four per warp (measured +7.6%, profiles/r2_reps.txt)
     "c2": ("C2: chat preset, 2000 req, lambda 12, 4 instances, capacity_fraction 0.3, pascal",
-           4736),
+           9472),
     "c1": ("C1: chat preset, 64 req, lambda 12, 1 instance, capacity_fraction 0.5, pascal", 4736),
     "c5": ("C5 slice: acceptance mixed 256 req, 4 instances, cap 0.5, lambda 2^(k/3) k=3..15, "
            "4 policies, seeds 0..", 4736),
